@@ -1,0 +1,206 @@
+/*
+ * oracle.c — plain, slow, fp64 CPU oracle for exact multi-head self-attention.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load or call this file.  It shares no
+ * code, header, table or helper with the CUDA path (paper_2405_15780_b200/), and
+ * neither side includes or imports the other.
+ *
+ * What it computes (the plain definition the method reaches up to rounding):
+ *   PAPER.md P:165 (§2.5, "Sequence Parallel (SP)"): after the all-to-all each GPU
+ *     holds "a complete sequence, but only for a non-overlapping subset of the
+ *     attention heads" and computes ordinary attention for those heads.
+ *   PAPER.md P:173-175 (§2.6, "Flash Attention v2"): FlashAttention tiles the
+ *     attention matrix; it is exact, so its result is the dense definition.
+ *   SPEC.md S:176 (mha_forward): out_h = softmax(Q_h K_h^T * scale) V_h,
+ *     scale = 1/sqrt(d_h); S:181-183 (mha_backward, analytic gradients);
+ *     S:188 (the tiled forward also returns the per-row logsumexp);
+ *     S:211-212 (no causal mask, no bias).
+ *
+ * Definitions, per batch b, head h, query row i, key row j (no blocking, no
+ * online rescaling — a two-pass max/sum per row):
+ *   s_ij  = scale * sum_d q[i,d] k[j,d]
+ *   m_i   = max_j s_ij
+ *   l_i   = sum_j exp(s_ij - m_i)
+ *   lse_i = m_i + ln l_i                    (natural log of the scaled scores)
+ *   P_ij  = exp(s_ij - lse_i)
+ *   o_i   = sum_j P_ij v_j
+ * Backward (standard softmax-attention calculus):
+ *   dV_j  = sum_i P_ij dO_i
+ *   dP_ij = dO_i . v_j
+ *   Delta_i = dO_i . o_i                    (with the oracle's own fp64 o_i)
+ *   dS_ij = P_ij (dP_ij - Delta_i)
+ *   dQ_i  = scale sum_j dS_ij k_j
+ *   dK_j  = scale sum_i dS_ij q_i
+ *
+ * Layouts (all contiguous, row-major, fp64):
+ *   q, out, dout, dq          [B][Nq][H][D]
+ *   k, v, dk, dv              [B][Nk][H][D]
+ *   lse                       [B][H][Nq]
+ * Self-attention is Nq == Nk; Nq != Nk serves the segment (LSS) tests, where a
+ * query block attends to a contiguous key segment only.
+ *
+ * Parity pins live in tests/test_oracle.py (brute force, finite differences,
+ * closed forms, invariants).  Every function here is pinned.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+static double dot(const double* a, const double* b, int64_t D) {
+  double acc = 0.0;
+  for (int64_t d = 0; d < D; ++d) acc += a[d] * b[d];
+  return acc;
+}
+
+int oracle_num_threads(void) {
+#ifdef _OPENMP
+  return omp_get_max_threads();
+#else
+  return 1;
+#endif
+}
+
+/* Forward for one query vector qi against keys/values of one (b, h).
+ * kb/vb point at key 0 of that (b, h); consecutive keys are rs = H*D apart.
+ * s is caller scratch of length Nk.  Writes o (D values) and returns lse. */
+static double attend_row(const double* qi, const double* kb, const double* vb,
+                         int64_t Nk, int64_t rs, int64_t D, double scale,
+                         double* s, double* o) {
+  double m = -INFINITY;
+  for (int64_t j = 0; j < Nk; ++j) {
+    s[j] = scale * dot(qi, kb + j * rs, D);
+    if (s[j] > m) m = s[j];
+  }
+  double l = 0.0;
+  for (int64_t j = 0; j < Nk; ++j) l += exp(s[j] - m);
+  double lse = m + log(l);
+  for (int64_t d = 0; d < D; ++d) o[d] = 0.0;
+  for (int64_t j = 0; j < Nk; ++j) {
+    double p = exp(s[j] - lse);
+    const double* vj = vb + j * rs;
+    for (int64_t d = 0; d < D; ++d) o[d] += p * vj[d];
+  }
+  return lse;
+}
+
+/* Dense forward: out [B][Nq][H][D], lse [B][H][Nq]. */
+void oracle_attn_fwd(const double* q, const double* k, const double* v,
+                     int64_t B, int64_t Nq, int64_t Nk, int64_t H, int64_t D,
+                     double* out, double* lse) {
+  const double scale = 1.0 / sqrt((double)D);
+  const int64_t rs = H * D;
+  const int64_t total = B * H * Nq;
+#pragma omp parallel
+  {
+    double* s = (double*)malloc(sizeof(double) * (size_t)(Nk > 0 ? Nk : 1));
+#pragma omp for schedule(static)
+    for (int64_t t = 0; t < total; ++t) {
+      int64_t b = t / (H * Nq), h = (t / Nq) % H, i = t % Nq;
+      const double* qi = q + ((b * Nq + i) * H + h) * D;
+      const double* kb = k + (b * Nk * H + h) * D;
+      const double* vb = v + (b * Nk * H + h) * D;
+      double* oi = out + ((b * Nq + i) * H + h) * D;
+      lse[(b * H + h) * Nq + i] = attend_row(qi, kb, vb, Nk, rs, D, scale, s, oi);
+    }
+    free(s);
+  }
+}
+
+/* Forward for an explicit list of R query vectors.  qrows [R][D]; row r belongs
+ * to (batch bh[2r], head bh[2r+1]) of k, v [B][Nk][H][D].  out_rows [R][D],
+ * lse_rows [R].  Each o_i depends only on q_i, K and V, so this is the exact
+ * forward for those rows (used for sampled checks at large N). */
+void oracle_attn_fwd_rows(const double* qrows, const int64_t* bh, int64_t R,
+                          const double* k, const double* v,
+                          int64_t B, int64_t Nk, int64_t H, int64_t D,
+                          double* out_rows, double* lse_rows) {
+  (void)B;
+  const double scale = 1.0 / sqrt((double)D);
+  const int64_t rs = H * D;
+#pragma omp parallel
+  {
+    double* s = (double*)malloc(sizeof(double) * (size_t)(Nk > 0 ? Nk : 1));
+#pragma omp for schedule(dynamic, 1)
+    for (int64_t r = 0; r < R; ++r) {
+      int64_t b = bh[2 * r], h = bh[2 * r + 1];
+      const double* kb = k + (b * Nk * H + h) * D;
+      const double* vb = v + (b * Nk * H + h) * D;
+      lse_rows[r] = attend_row(qrows + r * D, kb, vb, Nk, rs, D, scale, s, out_rows + r * D);
+    }
+    free(s);
+  }
+}
+
+/* Dense backward (self-attention, Nq == Nk == N).  Recomputes the forward in
+ * fp64 (pass 1), then dQ by rows (pass 2), then dK, dV by keys (pass 3) so no
+ * two threads write the same output.  out/lse receive the fp64 forward. */
+void oracle_attn_bwd(const double* q, const double* k, const double* v,
+                     const double* dout, int64_t B, int64_t N, int64_t H, int64_t D,
+                     double* dq, double* dk, double* dv, double* out, double* lse) {
+  const double scale = 1.0 / sqrt((double)D);
+  const int64_t rs = H * D;
+  const int64_t total = B * H * N;
+  double* delta = (double*)malloc(sizeof(double) * (size_t)(total > 0 ? total : 1));
+
+  /* pass 1: forward, and Delta_i = dO_i . o_i */
+#pragma omp parallel
+  {
+    double* s = (double*)malloc(sizeof(double) * (size_t)(N > 0 ? N : 1));
+#pragma omp for schedule(static)
+    for (int64_t t = 0; t < total; ++t) {
+      int64_t b = t / (H * N), h = (t / N) % H, i = t % N;
+      const int64_t ro = ((b * N + i) * H + h) * D;
+      const double* kb = k + (b * N * H + h) * D;
+      const double* vb = v + (b * N * H + h) * D;
+      lse[(b * H + h) * N + i] = attend_row(q + ro, kb, vb, N, rs, D, scale, s, out + ro);
+      delta[(b * H + h) * N + i] = dot(dout + ro, out + ro, D);
+    }
+    free(s);
+  }
+
+  /* pass 2: dQ_i = scale * sum_j P_ij (dO_i . v_j - Delta_i) k_j */
+#pragma omp parallel for schedule(static)
+  for (int64_t t = 0; t < total; ++t) {
+    int64_t b = t / (H * N), h = (t / N) % H, i = t % N;
+    const int64_t ro = ((b * N + i) * H + h) * D;
+    const double li = lse[(b * H + h) * N + i];
+    const double di = delta[(b * H + h) * N + i];
+    double* dqi = dq + ro;
+    for (int64_t d = 0; d < D; ++d) dqi[d] = 0.0;
+    for (int64_t j = 0; j < N; ++j) {
+      const double* kj = k + ((b * N + j) * H + h) * D;
+      const double* vj = v + ((b * N + j) * H + h) * D;
+      double p = exp(scale * dot(q + ro, kj, D) - li);
+      double ds = p * (dot(dout + ro, vj, D) - di);
+      for (int64_t d = 0; d < D; ++d) dqi[d] += ds * kj[d];
+    }
+    for (int64_t d = 0; d < D; ++d) dqi[d] *= scale;
+  }
+
+  /* pass 3: dV_j = sum_i P_ij dO_i ; dK_j = scale * sum_i dS_ij q_i */
+#pragma omp parallel for schedule(static)
+  for (int64_t t = 0; t < total; ++t) {
+    int64_t b = t / (H * N), h = (t / N) % H, j = t % N;
+    const int64_t rj = ((b * N + j) * H + h) * D;
+    double* dkj = dk + rj;
+    double* dvj = dv + rj;
+    for (int64_t d = 0; d < D; ++d) { dkj[d] = 0.0; dvj[d] = 0.0; }
+    for (int64_t i = 0; i < N; ++i) {
+      const int64_t ri = ((b * N + i) * H + h) * D;
+      double p = exp(scale * dot(q + ri, k + rj, D) - lse[(b * H + h) * N + i]);
+      double ds = p * (dot(dout + ri, v + rj, D) - delta[(b * H + h) * N + i]);
+      for (int64_t d = 0; d < D; ++d) {
+        dvj[d] += p * dout[ri + d];
+        dkj[d] += ds * q[ri + d];
+      }
+    }
+    for (int64_t d = 0; d < D; ++d) dkj[d] *= scale;
+  }
+  free(delta);
+}
