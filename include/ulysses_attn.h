@@ -1,0 +1,137 @@
+/*
+ * ulysses_attn.h — C ABI of the B200-native Ulysses sequence-parallel exact
+ * attention library (libulysses_attn.so).
+ *
+ * What it computes.  PAPER.md P:165 (§2.5, "Sequence Parallel (SP)"):
+ * DeepSpeed-Ulysses "partitions the input data along the sequence dimension",
+ * then "employs an all-to-all collective communication to ensure that each GPU
+ * receives a complete sequence, but only for a non-overlapping subset of the
+ * attention heads", computes attention for those heads, and a second
+ * all-to-all returns the result to sequence shards.  P:425 (§6.1): "two
+ * all-to-all calls in the forward pass and two all-to-all calls + all reduce in
+ * the backward pass per layer" (the all-reduce syncs weight gradients of the
+ * model's projections; this op has no weights, so it issues exactly 2 + 2).
+ * The local attention is exact softmax(Q K^T / sqrt(D)) V computed tile by
+ * tile with an online softmax (§2.6 FlashAttention-2), so the N x N
+ * score matrix never exists in memory.  No mask, no dropout, no bias.
+ *
+ * Conventions (all entry points):
+ *  - Every tensor is caller-owned device memory (cudaMalloc / torch), dense
+ *    row-major, 16-byte aligned.  The library never frees caller memory.
+ *  - bf16 = IEEE bfloat16 (uint16 storage); fp32 = float.
+ *  - Rank r of P owns tokens [r*N/P, (r+1)*N/P) ("sequence shard") and,
+ *    after the all-to-all, heads [r*H/P, (r+1)*H/P) ("head shard").
+ *  - scale = 1/sqrt(D); lse is the natural-log logsumexp of the scaled scores.
+ *  - Calls are asynchronous and stream-ordered on `stream`.  For P > 1 they are
+ *    COLLECTIVE: all P ranks call with identical (B, N, H, D, P) in the same
+ *    order.  Argument validation happens on the host before anything is
+ *    enqueued, so an invalid call returns the same status on every rank and
+ *    never hangs a peer.
+ *  - Errors: a non-UA_OK status; ua_last_error() returns a thread-local
+ *    human-readable detail.  Asynchronous CUDA / NCCL faults surface as
+ *    UA_ERR_CUDA / UA_ERR_NCCL on a later call.
+ *  - There is no CPU fallback: without an sm_100 device every compute entry
+ *    point fails with UA_ERR_UNSUPPORTED.
+ */
+#ifndef ULYSSES_ATTN_H_
+#define ULYSSES_ATTN_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct ua_ctx ua_ctx; /* opaque: rank, P, device, NCCL communicator */
+typedef struct CUstream_st* ua_stream_t; /* == cudaStream_t; NULL = legacy default stream */
+
+typedef enum {
+  UA_OK = 0,
+  UA_ERR_INVALID_ARG = 1,       /* null / misaligned pointer, non-positive size, P != ctx P, workspace too small */
+  UA_ERR_HEAD_DIVISIBILITY = 2, /* P > H or H % P != 0 (P:317 head limit) */
+  UA_ERR_SEQ_DIVISIBILITY = 3,  /* N % P != 0; no padding */
+  UA_ERR_UNSUPPORTED = 4,       /* D not in {32, 64, 128}; N >= 2^31; no sm_100 device */
+  UA_ERR_CUDA = 5,
+  UA_ERR_NCCL = 6
+} ua_status;
+
+/* Library version string, e.g. "ulysses_attn 0.1 sm_100a". Never NULL. */
+const char* ua_version(void);
+const char* ua_status_string(ua_status s);
+/* Detail of the last error on the calling thread ("" if none). */
+const char* ua_last_error(void);
+
+/* ------------------------------------------------------------- validation
+ * Pure host check of a problem shape, no device access (S:238, S:244, S:248,
+ * S:276).  Checked in this order: B, N, H, D, P >= 1 else
+ * INVALID_ARG; P > H or H % P else HEAD_DIVISIBILITY; N % P else
+ * SEQ_DIVISIBILITY; D not in {32,64,128} or N >= 2^31 else UNSUPPORTED. */
+ua_status ua_validate(int64_t B, int64_t N, int H, int D, int P);
+
+/* Workspace bytes the fwd / bwd calls need for this shape (0 for the forward
+ * at P == 1).  Either output pointer may be NULL. */
+ua_status ua_workspace_size(int64_t B, int64_t N, int H, int D, int P, size_t* fwd_bytes, size_t* bwd_bytes);
+
+/* ------------------------------------------------------------- context
+ * ua_get_unique_id: rank 0 creates a 128-byte NCCL unique id; the caller
+ * broadcasts it to the other ranks (e.g. over a torch.distributed group).
+ * ua_ctx_create: binds the calling thread to `cuda_device` and, for P > 1,
+ * creates the library's own NCCL communicator (ncclCommInitRank); `uid` is
+ * ignored (may be NULL) when P == 1.  The ctx owns that communicator and is
+ * released by ua_ctx_destroy. */
+ua_status ua_get_unique_id(unsigned char uid[128]);
+ua_status ua_ctx_create(const unsigned char* uid, int P, int rank, int cuda_device, ua_ctx** out);
+ua_status ua_ctx_destroy(ua_ctx* ctx);
+/* Per-ctx counters of collective traffic since creation (S:107-110 ledger):
+ * a2a calls (a fused Q/K/V exchange counts as one call) and bytes this
+ * rank sent to OTHER ranks. Either pointer may be NULL. */
+ua_status ua_ctx_comm_stats(const ua_ctx* ctx, int64_t* a2a_calls, int64_t* a2a_bytes_sent);
+
+/* ------------------------------------------------------------- forward
+ * q, k, v : bf16 [B][N/P][H][D]   this rank's sequence shard (inputs)
+ * out     : bf16 [B][N/P][H][D]   attention output, same shard (written)
+ * lse     : fp32 [B][H/P][N]      logsumexp of this rank's HEAD shard over
+ *                                 the full sequence (written; consumed by bwd)
+ * workspace: device scratch of at least ua_workspace_size(...).fwd_bytes
+ * P == 1: no communication; the kernels read q/k/v and write out in place.
+ * P > 1 : pack -> all-to-all #1 (fused q,k,v) -> attention -> all-to-all #2
+ *         -> unpack.  out must not alias q, k, v. */
+ua_status ua_ulysses_attn_fwd(ua_ctx* ctx, const void* q, const void* k, const void* v, void* out, float* lse,
+                              int64_t B, int64_t N, int H, int D, int P, void* workspace, size_t workspace_bytes,
+                              ua_stream_t stream);
+
+/* ------------------------------------------------------------- backward
+ * Inputs: q, k, v, out, dout bf16 [B][N/P][H][D] (sequence shard; out is the
+ * forward's output), lse fp32 [B][H/P][N] from the forward.
+ * Outputs: dq, dk, dv bf16 [B][N/P][H][D] (gradients of the loss w.r.t. this
+ * rank's shard of q, k, v).
+ * Delta = rowsum(dout * out) is formed in fp32 in sequence space and shipped
+ * with the all-to-all, so the backward needs no saved head-sharded state.
+ * P > 1: pack(+Delta) -> all-to-all #3 -> attention bwd -> all-to-all #4 ->
+ * unpack.  Outputs must not alias inputs. */
+ua_status ua_ulysses_attn_bwd(ua_ctx* ctx, const void* q, const void* k, const void* v, const void* out,
+                              const float* lse, const void* dout, void* dq, void* dk, void* dv, int64_t B, int64_t N,
+                              int H, int D, int P, void* workspace, size_t workspace_bytes, ua_stream_t stream);
+
+/* ------------------------------------------------------------- LSS chunking
+ * One contiguous key segment ("Long Sequence Segmentation"):
+ * exact attention of all N queries of a head-sharded problem over keys
+ * [kv_begin, kv_end) only.  Operates on head-layout tensors (no comm):
+ *   q, k, v : bf16 [B][N][Hx][D]   (Hx heads, e.g. one rank's head shard)
+ *   o_seg   : fp32 [B][Hx][N][D]   segment output, normalised over the segment
+ *   lse_seg : fp32 [B][Hx][N]      segment logsumexp
+ * kv_begin must be a multiple of 128; 0 <= kv_begin < kv_end <= N. */
+ua_status ua_attn_fwd_segment(const void* q, const void* k, const void* v, float* o_seg, float* lse_seg, int64_t B,
+                              int64_t N, int Hx, int D, int64_t kv_begin, int64_t kv_end, ua_stream_t stream);
+/* Exact merge (in place into a): lse_a <- logaddexp(lse_a, lse_b),
+ * o_a <- e^{lse_a_old - lse} o_a + e^{lse_b - lse} o_b.  rows = B*Hx*N. */
+ua_status ua_lse_merge(float* o_a, float* lse_a, const float* o_b, const float* lse_b, int64_t rows, int D,
+                       ua_stream_t stream);
+/* fp32 [B][Hx][N][D] -> bf16 [B][N][Hx][D] (final cast of a merged result). */
+ua_status ua_f32_to_bf16_bnhd(const float* src, void* dst, int64_t B, int64_t N, int Hx, int D, ua_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ULYSSES_ATTN_H_ */

@@ -53,10 +53,10 @@ def _load():
             lib = ctypes.CDLL(_LIB)
             d = ctypes.POINTER(ctypes.c_double)
             i64 = ctypes.c_int64
-            lib.oracle_attn_fwd.argtypes = [d, d, d, i64, i64, i64, i64, i64, d, d]
+            lib.oracle_attn_fwd.argtypes = [d, d, d, i64, i64, i64, i64, i64, d, d, d]
             lib.oracle_attn_fwd_rows.argtypes = [d, ctypes.POINTER(i64), i64, d, d,
                                                  i64, i64, i64, i64, d, d]
-            lib.oracle_attn_bwd.argtypes = [d, d, d, d, i64, i64, i64, i64, d, d, d, d, d]
+            lib.oracle_attn_bwd.argtypes = [d, d, d, d, i64, i64, i64, i64, d, d, d, d, d, d]
             lib.oracle_num_threads.restype = ctypes.c_int
             _lib = lib
     return _lib
@@ -74,18 +74,21 @@ def num_threads() -> int:
     return int(_load().oracle_num_threads())
 
 
-def attn_fwd(q, k, v):
+def attn_fwd(q, k, v, with_abs: bool = False):
     """Dense exact attention.  q [B][Nq][H][D], k/v [B][Nk][H][D] (fp64, any
     values; callers pass bf16-rounded inputs widened exactly).  Returns
-    (out [B][Nq][H][D], lse [B][H][Nq]) in fp64."""
+    (out [B][Nq][H][D], lse [B][H][Nq]) in fp64; with_abs=True appends
+    absv = sum_j P_ij |v_jd| (error-scale helper for the tests)."""
     q, k, v = _f64(q), _f64(k), _f64(v)
     B, Nq, H, D = q.shape
     Nk = k.shape[1]
     assert k.shape == (B, Nk, H, D) and v.shape == k.shape
     out = np.empty_like(q)
     lse = np.empty((B, H, Nq), dtype=np.float64)
-    _load().oracle_attn_fwd(_ptr(q), _ptr(k), _ptr(v), B, Nq, Nk, H, D, _ptr(out), _ptr(lse))
-    return out, lse
+    absv = np.empty_like(q) if with_abs else None
+    _load().oracle_attn_fwd(_ptr(q), _ptr(k), _ptr(v), B, Nq, Nk, H, D, _ptr(out), _ptr(lse),
+                            _ptr(absv) if with_abs else None)
+    return (out, lse, absv) if with_abs else (out, lse)
 
 
 def attn_fwd_rows(qrows, bh, k, v):
@@ -103,15 +106,21 @@ def attn_fwd_rows(qrows, bh, k, v):
     return out, lse
 
 
-def attn_bwd(q, k, v, dout):
-    """Dense exact backward (self-attention).  Returns (dq, dk, dv, out, lse)."""
+def attn_bwd(q, k, v, dout, with_abs: bool = False):
+    """Dense exact backward (self-attention).  Returns (dq, dk, dv, out, lse);
+    with_abs=True appends (dq_abs, dk_abs, dv_abs), the error-scale sums of
+    oracle.c (|dS|.|K|, |dS|^T.|Q| scaled, P^T.|dO|) used for tolerances."""
     q, k, v, dout = _f64(q), _f64(k), _f64(v), _f64(dout)
     B, N, H, D = q.shape
     assert k.shape == q.shape and v.shape == q.shape and dout.shape == q.shape
     dq, dk, dv, out = (np.empty_like(q) for _ in range(4))
     lse = np.empty((B, H, N), dtype=np.float64)
+    gabs = np.empty((3,) + q.shape, dtype=np.float64) if with_abs else None
     _load().oracle_attn_bwd(_ptr(q), _ptr(k), _ptr(v), _ptr(dout), B, N, H, D,
-                            _ptr(dq), _ptr(dk), _ptr(dv), _ptr(out), _ptr(lse))
+                            _ptr(dq), _ptr(dk), _ptr(dv), _ptr(out), _ptr(lse),
+                            _ptr(gabs) if with_abs else None)
+    if with_abs:
+        return dq, dk, dv, out, lse, (gabs[0], gabs[1], gabs[2])
     return dq, dk, dv, out, lse
 
 

@@ -68,10 +68,13 @@ int oracle_num_threads(void) {
 
 /* Forward for one query vector qi against keys/values of one (b, h).
  * kb/vb point at key 0 of that (b, h); consecutive keys are rs = H*D apart.
- * s is caller scratch of length Nk.  Writes o (D values) and returns lse. */
+ * s is caller scratch of length Nk.  Writes o (D values) and returns lse.
+ * If oabs != NULL it also writes sum_j P_ij |v_jd| — not part of the method:
+ * the magnitude a rounding error in P_ij is multiplied by, used by the tests
+ * to scale elementwise tolerances (equals o when V >= 0). */
 static double attend_row(const double* qi, const double* kb, const double* vb,
                          int64_t Nk, int64_t rs, int64_t D, double scale,
-                         double* s, double* o) {
+                         double* s, double* o, double* oabs) {
   double m = -INFINITY;
   for (int64_t j = 0; j < Nk; ++j) {
     s[j] = scale * dot(qi, kb + j * rs, D);
@@ -81,18 +84,23 @@ static double attend_row(const double* qi, const double* kb, const double* vb,
   for (int64_t j = 0; j < Nk; ++j) l += exp(s[j] - m);
   double lse = m + log(l);
   for (int64_t d = 0; d < D; ++d) o[d] = 0.0;
+  if (oabs)
+    for (int64_t d = 0; d < D; ++d) oabs[d] = 0.0;
   for (int64_t j = 0; j < Nk; ++j) {
     double p = exp(s[j] - lse);
     const double* vj = vb + j * rs;
     for (int64_t d = 0; d < D; ++d) o[d] += p * vj[d];
+    if (oabs)
+      for (int64_t d = 0; d < D; ++d) oabs[d] += p * fabs(vj[d]);
   }
   return lse;
 }
 
-/* Dense forward: out [B][Nq][H][D], lse [B][H][Nq]. */
+/* Dense forward: out [B][Nq][H][D], lse [B][H][Nq]; out_abs (nullable)
+ * [B][Nq][H][D] receives sum_j P_ij |v_jd| (see attend_row). */
 void oracle_attn_fwd(const double* q, const double* k, const double* v,
                      int64_t B, int64_t Nq, int64_t Nk, int64_t H, int64_t D,
-                     double* out, double* lse) {
+                     double* out, double* lse, double* out_abs) {
   const double scale = 1.0 / sqrt((double)D);
   const int64_t rs = H * D;
   const int64_t total = B * H * Nq;
@@ -106,7 +114,8 @@ void oracle_attn_fwd(const double* q, const double* k, const double* v,
       const double* kb = k + (b * Nk * H + h) * D;
       const double* vb = v + (b * Nk * H + h) * D;
       double* oi = out + ((b * Nq + i) * H + h) * D;
-      lse[(b * H + h) * Nq + i] = attend_row(qi, kb, vb, Nk, rs, D, scale, s, oi);
+      double* ai = out_abs ? out_abs + ((b * Nq + i) * H + h) * D : NULL;
+      lse[(b * H + h) * Nq + i] = attend_row(qi, kb, vb, Nk, rs, D, scale, s, oi, ai);
     }
     free(s);
   }
@@ -131,7 +140,7 @@ void oracle_attn_fwd_rows(const double* qrows, const int64_t* bh, int64_t R,
       int64_t b = bh[2 * r], h = bh[2 * r + 1];
       const double* kb = k + (b * Nk * H + h) * D;
       const double* vb = v + (b * Nk * H + h) * D;
-      lse_rows[r] = attend_row(qrows + r * D, kb, vb, Nk, rs, D, scale, s, out_rows + r * D);
+      lse_rows[r] = attend_row(qrows + r * D, kb, vb, Nk, rs, D, scale, s, out_rows + r * D, NULL);
     }
     free(s);
   }
@@ -139,14 +148,25 @@ void oracle_attn_fwd_rows(const double* qrows, const int64_t* bh, int64_t R,
 
 /* Dense backward (self-attention, Nq == Nk == N).  Recomputes the forward in
  * fp64 (pass 1), then dQ by rows (pass 2), then dK, dV by keys (pass 3) so no
- * two threads write the same output.  out/lse receive the fp64 forward. */
+ * two threads write the same output.  out/lse receive the fp64 forward.
+ * gabs (nullable, [3][B][N][H][D]) receives the error-scale sums the tests use
+ * for elementwise tolerances — not part of the method:
+ *   gabs[0] = scale sum_j (|dS_ij| + P_ij e_i) |k_j|,
+ *   gabs[1] = scale sum_i (|dS_ij| + P_ij e_i) |q_i|,
+ *   gabs[2] = sum_i P_ij |dO_i|,     e_i = sum_d |dO_id o_id|
+ * (the magnitudes that bf16 rounding of dS, P and of o inside Delta hits). */
 void oracle_attn_bwd(const double* q, const double* k, const double* v,
                      const double* dout, int64_t B, int64_t N, int64_t H, int64_t D,
-                     double* dq, double* dk, double* dv, double* out, double* lse) {
+                     double* dq, double* dk, double* dv, double* out, double* lse,
+                     double* gabs) {
   const double scale = 1.0 / sqrt((double)D);
   const int64_t rs = H * D;
   const int64_t total = B * H * N;
+  const int64_t nel = B * N * H * D;
   double* delta = (double*)malloc(sizeof(double) * (size_t)(total > 0 ? total : 1));
+  /* edelta_i = sum_d |dO_id o_id|: the size of the perturbation of Delta_i when
+   * o is rounded (error-scale helper only; used when gabs != NULL). */
+  double* edelta = (double*)malloc(sizeof(double) * (size_t)(total > 0 ? total : 1));
 
   /* pass 1: forward, and Delta_i = dO_i . o_i */
 #pragma omp parallel
@@ -158,8 +178,11 @@ void oracle_attn_bwd(const double* q, const double* k, const double* v,
       const int64_t ro = ((b * N + i) * H + h) * D;
       const double* kb = k + (b * N * H + h) * D;
       const double* vb = v + (b * N * H + h) * D;
-      lse[(b * H + h) * N + i] = attend_row(q + ro, kb, vb, N, rs, D, scale, s, out + ro);
+      lse[(b * H + h) * N + i] = attend_row(q + ro, kb, vb, N, rs, D, scale, s, out + ro, NULL);
       delta[(b * H + h) * N + i] = dot(dout + ro, out + ro, D);
+      double e = 0.0;
+      for (int64_t d = 0; d < D; ++d) e += fabs(dout[ro + d] * out[ro + d]);
+      edelta[(b * H + h) * N + i] = e;
     }
     free(s);
   }
@@ -172,15 +195,22 @@ void oracle_attn_bwd(const double* q, const double* k, const double* v,
     const double li = lse[(b * H + h) * N + i];
     const double di = delta[(b * H + h) * N + i];
     double* dqi = dq + ro;
+    double* aq = gabs ? gabs + ro : NULL;
     for (int64_t d = 0; d < D; ++d) dqi[d] = 0.0;
+    if (aq)
+      for (int64_t d = 0; d < D; ++d) aq[d] = 0.0;
     for (int64_t j = 0; j < N; ++j) {
       const double* kj = k + ((b * N + j) * H + h) * D;
       const double* vj = v + ((b * N + j) * H + h) * D;
       double p = exp(scale * dot(q + ro, kj, D) - li);
       double ds = p * (dot(dout + ro, vj, D) - di);
       for (int64_t d = 0; d < D; ++d) dqi[d] += ds * kj[d];
+      if (aq)
+        for (int64_t d = 0; d < D; ++d) aq[d] += (fabs(ds) + p * edelta[(b * H + h) * N + i]) * fabs(kj[d]);
     }
     for (int64_t d = 0; d < D; ++d) dqi[d] *= scale;
+    if (aq)
+      for (int64_t d = 0; d < D; ++d) aq[d] *= scale;
   }
 
   /* pass 3: dV_j = sum_i P_ij dO_i ; dK_j = scale * sum_i dS_ij q_i */
@@ -190,7 +220,11 @@ void oracle_attn_bwd(const double* q, const double* k, const double* v,
     const int64_t rj = ((b * N + j) * H + h) * D;
     double* dkj = dk + rj;
     double* dvj = dv + rj;
+    double* ak = gabs ? gabs + nel + rj : NULL;
+    double* av = gabs ? gabs + 2 * nel + rj : NULL;
     for (int64_t d = 0; d < D; ++d) { dkj[d] = 0.0; dvj[d] = 0.0; }
+    if (ak)
+      for (int64_t d = 0; d < D; ++d) { ak[d] = 0.0; av[d] = 0.0; }
     for (int64_t i = 0; i < N; ++i) {
       const int64_t ri = ((b * N + i) * H + h) * D;
       double p = exp(scale * dot(q + ri, k + rj, D) - lse[(b * H + h) * N + i]);
@@ -199,8 +233,16 @@ void oracle_attn_bwd(const double* q, const double* k, const double* v,
         dvj[d] += p * dout[ri + d];
         dkj[d] += ds * q[ri + d];
       }
+      if (ak)
+        for (int64_t d = 0; d < D; ++d) {
+          ak[d] += (fabs(ds) + p * edelta[(b * H + h) * N + i]) * fabs(q[ri + d]);
+          av[d] += p * fabs(dout[ri + d]);
+        }
     }
     for (int64_t d = 0; d < D; ++d) dkj[d] *= scale;
+    if (ak)
+      for (int64_t d = 0; d < D; ++d) ak[d] *= scale;
   }
   free(delta);
+  free(edelta);
 }

@@ -1,0 +1,277 @@
+"""Python binding of libulysses_attn.so (B200-native Ulysses sequence-parallel
+exact attention, arXiv 2405.15780).
+
+Argument marshalling only: every step of the hot path (pack, all-to-all,
+attention, unpack, Delta, dQ finalisation, LSE merge) runs inside the C-ABI
+library.  torch is used for device memory, streams and process groups.  There
+is no CPU fallback: importing works anywhere (so tests can check the library
+loads and exports its symbols), but every compute call raises if the CUDA
+extension is missing or no sm_100 device is present.
+
+Names follow include/ulysses_attn.h (§2.5).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libulysses_attn.so")
+
+UA_OK = 0
+STATUS = {0: "UA_OK", 1: "UA_ERR_INVALID_ARG", 2: "UA_ERR_HEAD_DIVISIBILITY", 3: "UA_ERR_SEQ_DIVISIBILITY",
+          4: "UA_ERR_UNSUPPORTED", 5: "UA_ERR_CUDA", 6: "UA_ERR_NCCL"}
+
+# Every symbol include/ulysses_attn.h declares.
+EXPORTS = ("ua_version", "ua_status_string", "ua_last_error", "ua_validate", "ua_workspace_size",
+           "ua_get_unique_id", "ua_ctx_create", "ua_ctx_destroy", "ua_ctx_comm_stats",
+           "ua_ulysses_attn_fwd", "ua_ulysses_attn_bwd", "ua_attn_fwd_segment", "ua_lse_merge",
+           "ua_f32_to_bf16_bnhd")
+
+
+class UlyssesError(RuntimeError):
+    def __init__(self, status: int, detail: str):
+        self.status = status
+        self.name = STATUS.get(status, f"status {status}")
+        super().__init__(f"{self.name}: {detail}")
+
+
+class HeadDivisibilityError(UlyssesError):
+    pass
+
+
+class SeqDivisibilityError(UlyssesError):
+    pass
+
+
+_lib = None
+
+
+def lib():
+    """Load libulysses_attn.so (fails loudly if it was not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} missing: run paper_2405_15780_b200/build.py (no CPU fallback exists)")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, i64, i32, sz = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_size_t
+        L.ua_version.restype = ctypes.c_char_p
+        L.ua_status_string.restype = ctypes.c_char_p
+        L.ua_status_string.argtypes = [i32]
+        L.ua_last_error.restype = ctypes.c_char_p
+        L.ua_validate.argtypes = [i64, i64, i32, i32, i32]
+        L.ua_workspace_size.argtypes = [i64, i64, i32, i32, i32, ctypes.POINTER(sz), ctypes.POINTER(sz)]
+        L.ua_get_unique_id.argtypes = [ctypes.c_char_p]
+        L.ua_ctx_create.argtypes = [ctypes.c_char_p, i32, i32, i32, ctypes.POINTER(vp)]
+        L.ua_ctx_destroy.argtypes = [vp]
+        L.ua_ctx_comm_stats.argtypes = [vp, ctypes.POINTER(i64), ctypes.POINTER(i64)]
+        L.ua_ulysses_attn_fwd.argtypes = [vp, vp, vp, vp, vp, vp, i64, i64, i32, i32, i32, vp, sz, vp]
+        L.ua_ulysses_attn_bwd.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, i64, i64, i32, i32, i32, vp, sz, vp]
+        L.ua_attn_fwd_segment.argtypes = [vp, vp, vp, vp, vp, i64, i64, i32, i32, i64, i64, vp]
+        L.ua_lse_merge.argtypes = [vp, vp, vp, vp, i64, i32, vp]
+        L.ua_f32_to_bf16_bnhd.argtypes = [vp, vp, i64, i64, i32, i32, vp]
+        for name in EXPORTS:
+            getattr(L, name).restype = getattr(L, name).restype if name in (
+                "ua_version", "ua_status_string", "ua_last_error") else i32
+        _lib = L
+    return _lib
+
+
+def _check(status: int):
+    if status != UA_OK:
+        detail = lib().ua_last_error().decode()
+        cls = {2: HeadDivisibilityError, 3: SeqDivisibilityError}.get(status, UlyssesError)
+        raise cls(status, detail)
+
+
+def version() -> str:
+    return lib().ua_version().decode()
+
+
+def validate(B: int, N: int, H: int, D: int, P: int) -> None:
+    """Host-only shape check (raises HeadDivisibilityError etc.)."""
+    _check(lib().ua_validate(B, N, H, D, P))
+
+
+def workspace_size(B: int, N: int, H: int, D: int, P: int) -> tuple[int, int]:
+    f, b = ctypes.c_size_t(0), ctypes.c_size_t(0)
+    _check(lib().ua_workspace_size(B, N, H, D, P, ctypes.byref(f), ctypes.byref(b)))
+    return f.value, b.value
+
+
+def get_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().ua_get_unique_id(buf))
+    return buf.raw
+
+
+def _ptr(t) -> ctypes.c_void_p:
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)
+
+
+def _stream(stream=None) -> ctypes.c_void_p:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _need_cuda_bf16(*ts):
+    for t in ts:
+        if not (t.is_cuda and t.dtype == torch.bfloat16 and t.is_contiguous()):
+            raise ValueError("expected contiguous bf16 CUDA tensors [B][N/P][H][D]")
+
+
+class Context:
+    """Owns a ua_ctx (and, for P > 1, the library's NCCL communicator).
+
+    For P > 1 pass ``group`` (a torch.distributed process group, any backend)
+    to broadcast rank 0's NCCL unique id; the data path never uses torch's
+    collectives."""
+
+    def __init__(self, P: int = 1, rank: int = 0, device: int | None = None, group=None, uid: bytes | None = None):
+        self.P, self.rank = P, rank
+        self.device = torch.cuda.current_device() if device is None else device
+        if P > 1 and uid is None:
+            import torch.distributed as dist
+            obj = [get_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0, group=group)
+            uid = obj[0]
+        h = ctypes.c_void_p(0)
+        _check(lib().ua_ctx_create(uid if P > 1 else None, P, rank, self.device, ctypes.byref(h)))
+        self._h = h
+        self._ws = {}
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if self._h and self._h.value:
+            _check(lib().ua_ctx_destroy(self._h))
+            self._h = ctypes.c_void_p(0)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def comm_stats(self) -> tuple[int, int]:
+        c, b = ctypes.c_int64(0), ctypes.c_int64(0)
+        _check(lib().ua_ctx_comm_stats(self._h, ctypes.byref(c), ctypes.byref(b)))
+        return c.value, b.value
+
+    def workspace(self, nbytes: int) -> torch.Tensor:
+        """Cached device workspace of at least nbytes."""
+        ws = self._ws.get("buf")
+        if ws is None or ws.numel() < nbytes:
+            ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=f"cuda:{self.device}")
+            self._ws["buf"] = ws
+        return ws
+
+
+@dataclass
+class FwdOut:
+    out: torch.Tensor
+    lse: torch.Tensor
+
+
+def ulysses_attn_fwd(ctx: Context, q, k, v, H: int | None = None, out=None, lse=None, stream=None) -> FwdOut:
+    """q, k, v: bf16 [B][N/P][H][D] (this rank's sequence shard).
+    Returns out [B][N/P][H][D] bf16 and lse [B][H/P][N] fp32."""
+    _need_cuda_bf16(q, k, v)
+    B, Nl, H_, D = q.shape
+    P = ctx.P
+    N = Nl * P
+    if out is None:
+        out = torch.empty_like(q)
+    if lse is None:
+        lse = torch.empty((B, H_ // P if H_ % P == 0 else 1, N), dtype=torch.float32, device=q.device)
+    validate(B, N, H_, D, P)
+    fb, _ = workspace_size(B, N, H_, D, P)
+    ws = ctx.workspace(fb)
+    _check(lib().ua_ulysses_attn_fwd(ctx.handle, _ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(lse), B, N, H_, D, P,
+                                     _ptr(ws), ws.numel(), _stream(stream)))
+    return FwdOut(out, lse)
+
+
+def ulysses_attn_bwd(ctx: Context, q, k, v, out, lse, dout, dq=None, dk=None, dv=None, stream=None):
+    """Gradients (dq, dk, dv) bf16 [B][N/P][H][D] of this rank's shard."""
+    _need_cuda_bf16(q, k, v, out, dout)
+    B, Nl, H, D = q.shape
+    P = ctx.P
+    N = Nl * P
+    dq = torch.empty_like(q) if dq is None else dq
+    dk = torch.empty_like(k) if dk is None else dk
+    dv = torch.empty_like(v) if dv is None else dv
+    validate(B, N, H, D, P)
+    _, bb = workspace_size(B, N, H, D, P)
+    ws = ctx.workspace(bb)
+    _check(lib().ua_ulysses_attn_bwd(ctx.handle, _ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(lse), _ptr(dout),
+                                     _ptr(dq), _ptr(dk), _ptr(dv), B, N, H, D, P, _ptr(ws), ws.numel(),
+                                     _stream(stream)))
+    return dq, dk, dv
+
+
+def attn_fwd_segment(q, k, v, kv_begin: int, kv_end: int, o_seg=None, lse_seg=None, stream=None):
+    """One LSS key segment on head-layout tensors q, k, v bf16 [B][N][Hx][D].
+    Returns (o_seg fp32 [B][Hx][N][D], lse_seg fp32 [B][Hx][N])."""
+    _need_cuda_bf16(q, k, v)
+    B, N, Hx, D = q.shape
+    if o_seg is None:
+        o_seg = torch.empty((B, Hx, N, D), dtype=torch.float32, device=q.device)
+    if lse_seg is None:
+        lse_seg = torch.empty((B, Hx, N), dtype=torch.float32, device=q.device)
+    _check(lib().ua_attn_fwd_segment(_ptr(q), _ptr(k), _ptr(v), _ptr(o_seg), _ptr(lse_seg), B, N, Hx, D, kv_begin,
+                                     kv_end, _stream(stream)))
+    return o_seg, lse_seg
+
+
+def lse_merge(o_a, lse_a, o_b, lse_b, stream=None):
+    """In-place exact merge of segment b into segment a."""
+    D = o_a.shape[-1]
+    _check(lib().ua_lse_merge(_ptr(o_a), _ptr(lse_a), _ptr(o_b), _ptr(lse_b), lse_a.numel(), D, _stream(stream)))
+    return o_a, lse_a
+
+
+def f32_to_bf16_bnhd(src, stream=None):
+    """fp32 [B][Hx][N][D] -> bf16 [B][N][Hx][D]."""
+    B, Hx, N, D = src.shape
+    dst = torch.empty((B, N, Hx, D), dtype=torch.bfloat16, device=src.device)
+    _check(lib().ua_f32_to_bf16_bnhd(_ptr(src), _ptr(dst), B, N, Hx, D, _stream(stream)))
+    return dst
+
+
+def lss_chunked_fwd(q, k, v, seg_len: int, stream=None):
+    """Exact attention over head-layout q, k, v [B][N][Hx][D] computed as
+    contiguous key segments of seg_len (multiple of 128) merged by LSE
+    (P:72).  Returns (out bf16 [B][N][Hx][D], lse fp32 [B][Hx][N])."""
+    B, N, Hx, D = q.shape
+    if seg_len % 128 != 0 or seg_len < 128:
+        raise ValueError("seg_len must be a positive multiple of 128")
+    o_acc, l_acc = attn_fwd_segment(q, k, v, 0, min(seg_len, N), stream=stream)
+    o_tmp = torch.empty_like(o_acc)
+    l_tmp = torch.empty_like(l_acc)
+    for j0 in range(seg_len, N, seg_len):
+        attn_fwd_segment(q, k, v, j0, min(j0 + seg_len, N), o_tmp, l_tmp, stream=stream)
+        lse_merge(o_acc, l_acc, o_tmp, l_tmp, stream=stream)
+    return f32_to_bf16_bnhd(o_acc, stream=stream), l_acc
+
+
+class UlyssesAttention(torch.autograd.Function):
+    """autograd wrapper: y = ulysses_attn(q, k, v) on this rank's shard."""
+
+    @staticmethod
+    def forward(ctx_, q, k, v, uctx: Context):
+        r = ulysses_attn_fwd(uctx, q, k, v)
+        ctx_.save_for_backward(q, k, v, r.out, r.lse)
+        ctx_.uctx = uctx
+        return r.out
+
+    @staticmethod
+    def backward(ctx_, dout):
+        q, k, v, out, lse = ctx_.saved_tensors
+        dq, dk, dv = ulysses_attn_bwd(ctx_.uctx, q, k, v, out, lse, dout.contiguous())
+        return dq, dk, dv, None

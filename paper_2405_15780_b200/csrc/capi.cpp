@@ -1,0 +1,482 @@
+// capi.cpp — the C ABI (include/ulysses_attn.h): validation, workspace plan,
+// NCCL all-to-all, and the launch sequence of the Ulysses forward / backward.
+#include "../../include/ulysses_attn.h"
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "kernels/attn_kernels.h"
+#include "tma_host.h"
+
+struct ua_ctx {
+  int P = 1;
+  int rank = 0;
+  int device = 0;
+  ncclComm_t comm = nullptr;
+  int64_t a2a_calls = 0;
+  int64_t a2a_bytes = 0;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+ua_status fail(ua_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return s;
+}
+
+#define UA_CUDA(expr)                                                                       \
+  do {                                                                                      \
+    cudaError_t e_ = (expr);                                                                \
+    if (e_ != cudaSuccess) return fail(UA_ERR_CUDA, "%s: %s", #expr, cudaGetErrorString(e_)); \
+  } while (0)
+
+#define UA_NCCL(expr)                                                                        \
+  do {                                                                                       \
+    ncclResult_t r_ = (expr);                                                                \
+    if (r_ != ncclSuccess) return fail(UA_ERR_NCCL, "%s: %s", #expr, ncclGetErrorString(r_)); \
+  } while (0)
+
+#define UA_TRY(expr)                  \
+  do {                                \
+    ua_status s_ = (expr);            \
+    if (s_ != UA_OK) return s_;       \
+  } while (0)
+
+constexpr size_t kAlign = 256;
+size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+ua_status check_device() {
+  static std::mutex mu;
+  static int checked[64] = {0};  // 0 unknown, 1 ok, 2 bad
+  int dev = -1;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess || dev < 0 || dev >= 64) {
+    cudaGetLastError();
+    return fail(UA_ERR_UNSUPPORTED, "no CUDA device available (%s); this library has no CPU fallback",
+                cudaGetErrorString(e));
+  }
+  std::lock_guard<std::mutex> lk(mu);
+  if (checked[dev] == 0) {
+    int major = 0, minor = 0;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+    cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+    checked[dev] = (major == 10 && minor == 0) ? 1 : 2;
+  }
+  if (checked[dev] != 1) return fail(UA_ERR_UNSUPPORTED, "device %d is not sm_100 (B200); kernels are sm_100a only", dev);
+  return UA_OK;
+}
+
+struct Shape {
+  int64_t B, N, Nl;
+  int H, Hl, D, P;
+  int64_t shard() const { return B * Nl * H * D; }  // elements of one [B][N/P][H][D] shard
+  int64_t chunk() const { return Nl * B * Hl * D; }  // elements per (tensor, peer) in the a2a
+};
+
+Shape make_shape(int64_t B, int64_t N, int H, int D, int P) {
+  Shape s;
+  s.B = B; s.N = N; s.H = H; s.D = D; s.P = P;
+  s.Nl = N / P; s.Hl = H / P;
+  return s;
+}
+
+// 4-D map {D, N, heads, B} over a bf16 view with token / head / batch strides (elements).
+ua_status make_map(CUtensorMap* m, const void* base, int D, int64_t N, int heads, int64_t B, int64_t sn, int64_t sh,
+                   int64_t sb) {
+  const uint64_t dims[4] = {uint64_t(D), uint64_t(N), uint64_t(heads), uint64_t(B)};
+  const uint64_t strides[3] = {uint64_t(sn) * 2, uint64_t(sh) * 2, uint64_t(sb) * 2};
+  const uint32_t box0 = D >= 64 ? 64 : uint32_t(D);
+  if (!ua::make_tmap_bf16_4d(m, base, dims, strides, box0, 128,
+                             D >= 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B))
+    return fail(UA_ERR_CUDA, "cuTensorMapEncodeTiled failed (D=%d N=%lld heads=%d)", D, (long long)N, heads);
+  return UA_OK;
+}
+
+// Workspace plans (byte offsets).
+struct FwdPlan {
+  size_t send = 0, recv = 0, o_head = 0, total = 0;
+};
+FwdPlan plan_fwd(const Shape& s) {
+  FwdPlan p;
+  if (s.P == 1) return p;
+  const size_t S = size_t(s.shard()) * 2;
+  p.send = 0;                         // [3][P][Nl][B][Hl][D]; reused as recv_o [P][Nl][B][Hl][D]
+  p.recv = align_up(p.send + 3 * S);  // [3][N][B][Hl][D]
+  p.o_head = align_up(p.recv + 3 * S);
+  p.total = align_up(p.o_head + S);
+  return p;
+}
+struct BwdPlan {
+  size_t send = 0, send_delta = 0, recv = 0, recv_delta = 0, dq_acc = 0, grad = 0, delta = 0, total = 0;
+};
+BwdPlan plan_bwd(const Shape& s) {
+  BwdPlan p;
+  const size_t S = size_t(s.shard()) * 2;
+  const size_t DL = size_t(s.B * s.Nl * s.H) * 4;  // Delta of one shard
+  const int64_t n_pad = (s.N + 127) / 128 * 128;
+  const size_t DQ = size_t(s.B * s.Hl * n_pad * s.D) * 4;  // fp32 dQ accumulator, rows padded to 128
+  if (s.P == 1) {
+    p.delta = 0;                                  // [N][B][H] fp32
+    p.dq_acc = align_up(DL);                      // [B*H][N_pad][D] fp32
+    p.total = align_up(p.dq_acc + DQ);
+    return p;
+  }
+  p.send = 0;                                     // [4][P][Nl][B][Hl][D]; reused as recv_grad [3][P]...
+  p.send_delta = align_up(4 * S);                 // [P][Nl][B][Hl]
+  p.recv = align_up(p.send_delta + DL);           // [4][N][B][Hl][D]
+  p.recv_delta = align_up(p.recv + 4 * S);        // [N][B][Hl]
+  p.dq_acc = align_up(p.recv_delta + DL);         // [B*Hl][N_pad][D] fp32
+  p.grad = align_up(p.dq_acc + DQ);               // [3][N][B][Hl][D] bf16
+  p.total = align_up(p.grad + 3 * S);
+  return p;
+}
+
+// Fused all-to-all of `nt` equally-shaped tensors: peer chunk i of tensor w is
+// `count` elements at send[w] + i*count (bytes elem_size).  One NCCL group =
+// one collective call in the S:274 sense.
+ua_status a2a(ua_ctx* ctx, void* const* send, void* const* recv, int nt, size_t count, ncclDataType_t dt,
+              size_t elem_size, cudaStream_t stream) {
+  UA_NCCL(ncclGroupStart());
+  for (int peer = 0; peer < ctx->P; ++peer) {
+    for (int w = 0; w < nt; ++w) {
+      const char* sp = static_cast<const char*>(send[w]) + size_t(peer) * count * elem_size;
+      char* rp = static_cast<char*>(recv[w]) + size_t(peer) * count * elem_size;
+      ncclResult_t r1 = ncclSend(sp, count, dt, peer, ctx->comm, stream);
+      ncclResult_t r2 = ncclRecv(rp, count, dt, peer, ctx->comm, stream);
+      if (r1 != ncclSuccess || r2 != ncclSuccess) {
+        ncclGroupEnd();
+        return fail(UA_ERR_NCCL, "ncclSend/Recv: %s", ncclGetErrorString(r1 != ncclSuccess ? r1 : r2));
+      }
+    }
+  }
+  UA_NCCL(ncclGroupEnd());
+  ctx->a2a_bytes += int64_t(ctx->P - 1) * int64_t(count * elem_size) * nt;
+  return UA_OK;
+}
+
+ua_status check_async(ua_ctx* ctx) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(UA_ERR_CUDA, "pending CUDA error: %s", cudaGetErrorString(e));
+  if (ctx && ctx->comm) {
+    ncclResult_t ar = ncclSuccess;
+    ncclCommGetAsyncError(ctx->comm, &ar);
+    if (ar != ncclSuccess) return fail(UA_ERR_NCCL, "NCCL async error: %s", ncclGetErrorString(ar));
+  }
+  return UA_OK;
+}
+
+ua_status launch_attention_fwd(const void* q, const void* k, const void* v, int64_t sn, int64_t sh, int64_t sb,
+                               ua::ViewArg o, float* o_f32, int64_t of_sn, int64_t of_sh, int64_t of_sb, float* lse,
+                               int64_t l_sh, int64_t l_sb, int64_t B, int64_t N, int heads, int D, int64_t kv_begin,
+                               int64_t kv_end, cudaStream_t stream) {
+  ua::FwdParams p;
+  std::memset(&p, 0, sizeof(p));
+  UA_TRY(make_map(&p.tm_q, q, D, N, heads, B, sn, sh, sb));
+  UA_TRY(make_map(&p.tm_k, k, D, N, heads, B, sn, sh, sb));
+  UA_TRY(make_map(&p.tm_v, v, D, N, heads, B, sn, sh, sb));
+  p.o = o;
+  p.o_f32 = o_f32;
+  p.of_sn = of_sn; p.of_sh = of_sh; p.of_sb = of_sb;
+  p.lse = lse;
+  p.l_sh = l_sh; p.l_sb = l_sb;
+  p.n_q = int(N);
+  p.kv_begin = int(kv_begin);
+  p.kv_end = int(kv_end);
+  p.scale_log2 = float(1.4426950408889634 / std::sqrt(double(D)));
+  UA_CUDA(ua::launch_attn_fwd(p, D, int(B), heads, stream));
+  return UA_OK;
+}
+
+ua_status launch_attention_bwd(const void* q, const void* k, const void* v, const void* dout, int64_t sn, int64_t sh,
+                               int64_t sb, ua::ViewArg dk, ua::ViewArg dv, float* dq_acc, const float* lse,
+                               int64_t l_sh, int64_t l_sb, const float* delta, int64_t d_sn, int64_t d_sh,
+                               int64_t d_sb, int64_t B, int64_t N, int heads, int D, cudaStream_t stream) {
+  ua::BwdParams p;
+  std::memset(&p, 0, sizeof(p));
+  UA_TRY(make_map(&p.tm_q, q, D, N, heads, B, sn, sh, sb));
+  UA_TRY(make_map(&p.tm_k, k, D, N, heads, B, sn, sh, sb));
+  UA_TRY(make_map(&p.tm_v, v, D, N, heads, B, sn, sh, sb));
+  UA_TRY(make_map(&p.tm_do, dout, D, N, heads, B, sn, sh, sb));
+  p.dk = dk;
+  p.dv = dv;
+  p.dq_acc = dq_acc;
+  p.lse = lse;
+  p.l_sh = l_sh; p.l_sb = l_sb;
+  p.delta = delta;
+  p.d_sn = d_sn; p.d_sh = d_sh; p.d_sb = d_sb;
+  p.n = int(N);
+  p.heads = heads;
+  p.scale = float(1.0 / std::sqrt(double(D)));
+  p.scale_log2 = float(1.4426950408889634 / std::sqrt(double(D)));
+  UA_CUDA(ua::launch_attn_bwd(p, D, int(B), heads, stream));
+  return UA_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ua_version(void) { return "ulysses_attn 0.1 sm_100a"; }
+
+const char* ua_status_string(ua_status s) {
+  switch (s) {
+    case UA_OK: return "UA_OK";
+    case UA_ERR_INVALID_ARG: return "UA_ERR_INVALID_ARG";
+    case UA_ERR_HEAD_DIVISIBILITY: return "UA_ERR_HEAD_DIVISIBILITY";
+    case UA_ERR_SEQ_DIVISIBILITY: return "UA_ERR_SEQ_DIVISIBILITY";
+    case UA_ERR_UNSUPPORTED: return "UA_ERR_UNSUPPORTED";
+    case UA_ERR_CUDA: return "UA_ERR_CUDA";
+    case UA_ERR_NCCL: return "UA_ERR_NCCL";
+  }
+  return "UA_ERR_UNKNOWN";
+}
+
+const char* ua_last_error(void) { return g_err.c_str(); }
+
+ua_status ua_validate(int64_t B, int64_t N, int H, int D, int P) {
+  if (B < 1 || N < 1 || H < 1 || D < 1 || P < 1)
+    return fail(UA_ERR_INVALID_ARG, "B, N, H, D, P must be >= 1 (got B=%lld N=%lld H=%d D=%d P=%d)", (long long)B,
+                (long long)N, H, D, P);
+  if (P > H || H % P != 0)
+    return fail(UA_ERR_HEAD_DIVISIBILITY, "Ulysses needs P <= H and H %% P == 0 (H=%d, P=%d)", H, P);
+  if (N % P != 0) return fail(UA_ERR_SEQ_DIVISIBILITY, "Ulysses needs N %% P == 0 (N=%lld, P=%d)", (long long)N, P);
+  if (D != 32 && D != 64 && D != 128) return fail(UA_ERR_UNSUPPORTED, "head dim D=%d not in {32, 64, 128}", D);
+  if (N >= (int64_t(1) << 31)) return fail(UA_ERR_UNSUPPORTED, "N=%lld >= 2^31", (long long)N);
+  if (B * N * H >= (int64_t(1) << 40)) return fail(UA_ERR_UNSUPPORTED, "problem too large");
+  return UA_OK;
+}
+
+ua_status ua_workspace_size(int64_t B, int64_t N, int H, int D, int P, size_t* fwd_bytes, size_t* bwd_bytes) {
+  UA_TRY(ua_validate(B, N, H, D, P));
+  Shape s = make_shape(B, N, H, D, P);
+  if (fwd_bytes) *fwd_bytes = plan_fwd(s).total;
+  if (bwd_bytes) *bwd_bytes = plan_bwd(s).total;
+  return UA_OK;
+}
+
+ua_status ua_get_unique_id(unsigned char uid[128]) {
+  if (!uid) return fail(UA_ERR_INVALID_ARG, "uid is NULL");
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  ncclUniqueId id;
+  UA_NCCL(ncclGetUniqueId(&id));
+  std::memcpy(uid, &id, 128);
+  return UA_OK;
+}
+
+ua_status ua_ctx_create(const unsigned char* uid, int P, int rank, int cuda_device, ua_ctx** out) {
+  if (!out) return fail(UA_ERR_INVALID_ARG, "out is NULL");
+  *out = nullptr;
+  if (P < 1 || rank < 0 || rank >= P) return fail(UA_ERR_INVALID_ARG, "bad P=%d rank=%d", P, rank);
+  if (P > 1 && !uid) return fail(UA_ERR_INVALID_ARG, "uid is NULL for P=%d", P);
+  UA_CUDA(cudaSetDevice(cuda_device));
+  UA_TRY(check_device());
+  ua_ctx* c = new ua_ctx();
+  c->P = P;
+  c->rank = rank;
+  c->device = cuda_device;
+  if (P > 1) {
+    ncclUniqueId id;
+    std::memcpy(&id, uid, 128);
+    ncclResult_t r = ncclCommInitRank(&c->comm, P, id, rank);
+    if (r != ncclSuccess) {
+      delete c;
+      return fail(UA_ERR_NCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
+    }
+  }
+  *out = c;
+  return UA_OK;
+}
+
+ua_status ua_ctx_destroy(ua_ctx* ctx) {
+  if (!ctx) return UA_OK;
+  ncclResult_t r = ncclSuccess;
+  if (ctx->comm) r = ncclCommDestroy(ctx->comm);
+  delete ctx;
+  if (r != ncclSuccess) return fail(UA_ERR_NCCL, "ncclCommDestroy: %s", ncclGetErrorString(r));
+  return UA_OK;
+}
+
+ua_status ua_ctx_comm_stats(const ua_ctx* ctx, int64_t* a2a_calls, int64_t* a2a_bytes_sent) {
+  if (!ctx) return fail(UA_ERR_INVALID_ARG, "ctx is NULL");
+  if (a2a_calls) *a2a_calls = ctx->a2a_calls;
+  if (a2a_bytes_sent) *a2a_bytes_sent = ctx->a2a_bytes;
+  return UA_OK;
+}
+
+ua_status ua_ulysses_attn_fwd(ua_ctx* ctx, const void* q, const void* k, const void* v, void* out, float* lse,
+                              int64_t B, int64_t N, int H, int D, int P, void* workspace, size_t workspace_bytes,
+                              ua_stream_t stream_) {
+  cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
+  UA_TRY(ua_validate(B, N, H, D, P));
+  if (!ctx) return fail(UA_ERR_INVALID_ARG, "ctx is NULL");
+  if (P != ctx->P) return fail(UA_ERR_INVALID_ARG, "P=%d differs from ctx P=%d", P, ctx->P);
+  if (!q || !k || !v || !out || !lse) return fail(UA_ERR_INVALID_ARG, "null tensor pointer");
+  if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(out) || !aligned16(lse))
+    return fail(UA_ERR_INVALID_ARG, "tensor pointers must be 16-byte aligned");
+  const Shape s = make_shape(B, N, H, D, P);
+  const FwdPlan plan = plan_fwd(s);
+  if (workspace_bytes < plan.total || (plan.total > 0 && !workspace))
+    return fail(UA_ERR_INVALID_ARG, "workspace too small: need %zu bytes, got %zu", plan.total, workspace_bytes);
+  UA_TRY(check_device());
+  UA_TRY(check_async(ctx));
+
+  if (P == 1) {
+    const int64_t sn = int64_t(H) * D, sh = D, sb = N * H * D;
+    ua::ViewArg o{out, sn, sh, sb};
+    return launch_attention_fwd(q, k, v, sn, sh, sb, o, nullptr, 0, 0, 0, lse, N, int64_t(H) * N, B, N, H, D, 0, N,
+                                stream);
+  }
+
+  char* ws = static_cast<char*>(workspace);
+  const size_t S = size_t(s.shard()) * 2;
+  void* send[3] = {ws + plan.send, ws + plan.send + S, ws + plan.send + 2 * S};
+  void* recv[3] = {ws + plan.recv, ws + plan.recv + S, ws + plan.recv + 2 * S};
+  const void* src[3] = {q, k, v};
+  // 1. pack (sequence shard -> per-destination head chunks)
+  UA_CUDA(ua::launch_pack(src, send, 3, B, s.Nl, H, D, P, nullptr, nullptr, nullptr, stream));
+  // 2. all-to-all #1 (fused q, k, v): rank j receives all N tokens of its head block
+  UA_TRY(a2a(ctx, send, recv, 3, size_t(s.chunk()), ncclBfloat16, 2, stream));
+  ctx->a2a_calls += 1;
+  // 3. attention on the head shard, layout [N][B][Hl][D]; O straight into the send layout of #2
+  const int64_t sn = B * int64_t(s.Hl) * D, sh = D, sb = int64_t(s.Hl) * D;
+  void* o_head = ws + plan.o_head;
+  ua::ViewArg o{o_head, sn, sh, sb};
+  UA_TRY(launch_attention_fwd(recv[0], recv[1], recv[2], sn, sh, sb, o, nullptr, 0, 0, 0, lse, N, int64_t(s.Hl) * N, B,
+                              N, s.Hl, D, 0, N, stream));
+  // 4. all-to-all #2: token block i of every local head goes back to rank i
+  void* recv_o = ws + plan.send;
+  UA_TRY(a2a(ctx, &o_head, &recv_o, 1, size_t(s.chunk()), ncclBfloat16, 2, stream));
+  ctx->a2a_calls += 1;
+  // 5. unpack head chunks -> [B][Nl][H][D]
+  const void* usrc[1] = {recv_o};
+  void* udst[1] = {out};
+  UA_CUDA(ua::launch_unpack(usrc, udst, 1, B, s.Nl, H, D, P, stream));
+  return UA_OK;
+}
+
+ua_status ua_ulysses_attn_bwd(ua_ctx* ctx, const void* q, const void* k, const void* v, const void* out,
+                              const float* lse, const void* dout, void* dq, void* dk, void* dv, int64_t B, int64_t N,
+                              int H, int D, int P, void* workspace, size_t workspace_bytes, ua_stream_t stream_) {
+  cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
+  UA_TRY(ua_validate(B, N, H, D, P));
+  if (!ctx) return fail(UA_ERR_INVALID_ARG, "ctx is NULL");
+  if (P != ctx->P) return fail(UA_ERR_INVALID_ARG, "P=%d differs from ctx P=%d", P, ctx->P);
+  const void* ptrs[] = {q, k, v, out, lse, dout, dq, dk, dv};
+  for (const void* ptr : ptrs) {
+    if (!ptr) return fail(UA_ERR_INVALID_ARG, "null tensor pointer");
+    if (!aligned16(ptr)) return fail(UA_ERR_INVALID_ARG, "tensor pointers must be 16-byte aligned");
+  }
+  const Shape s = make_shape(B, N, H, D, P);
+  const BwdPlan plan = plan_bwd(s);
+  if (workspace_bytes < plan.total || !workspace)
+    return fail(UA_ERR_INVALID_ARG, "workspace too small: need %zu bytes, got %zu", plan.total, workspace_bytes);
+  UA_TRY(check_device());
+  UA_TRY(check_async(ctx));
+  char* ws = static_cast<char*>(workspace);
+
+  if (P == 1) {
+    float* delta = reinterpret_cast<float*>(ws + plan.delta);
+    float* dq_acc = reinterpret_cast<float*>(ws + plan.dq_acc);
+    // Delta[n][b][h] = sum_d dO.O (fp32)
+    UA_CUDA(ua::launch_pack(nullptr, nullptr, 0, B, N, H, D, 1, dout, out, delta, stream));
+    UA_CUDA(cudaMemsetAsync(dq_acc, 0, size_t(B * H * ((N + 127) / 128 * 128) * D) * 4, stream));
+    const int64_t sn = int64_t(H) * D, sh = D, sb = N * H * D;
+    ua::ViewArg vdk{dk, sn, sh, sb}, vdv{dv, sn, sh, sb}, vdq{dq, sn, sh, sb};
+    UA_TRY(launch_attention_bwd(q, k, v, dout, sn, sh, sb, vdk, vdv, dq_acc, lse, N, int64_t(H) * N, delta,
+                                B * int64_t(H), 1, H, B, N, H, D, stream));
+    UA_CUDA(ua::launch_dq_finalize(dq_acc, vdq, B, N, H, D, float(1.0 / std::sqrt(double(D))), stream));
+    return UA_OK;
+  }
+
+  const size_t S = size_t(s.shard()) * 2;
+  void* send[4] = {ws + plan.send, ws + plan.send + S, ws + plan.send + 2 * S, ws + plan.send + 3 * S};
+  void* recv[4] = {ws + plan.recv, ws + plan.recv + S, ws + plan.recv + 2 * S, ws + plan.recv + 3 * S};
+  float* send_delta = reinterpret_cast<float*>(ws + plan.send_delta);
+  float* recv_delta = reinterpret_cast<float*>(ws + plan.recv_delta);
+  float* dq_acc = reinterpret_cast<float*>(ws + plan.dq_acc);
+  void* grad[3] = {ws + plan.grad, ws + plan.grad + S, ws + plan.grad + 2 * S};
+  const void* src[4] = {q, k, v, dout};
+  // 1. pack q, k, v, dO + Delta = rowsum(dO * O) in sequence space
+  UA_CUDA(ua::launch_pack(src, send, 4, B, s.Nl, H, D, P, dout, out, send_delta, stream));
+  // 2. all-to-all #3 (fused q, k, v, dO, Delta)
+  UA_NCCL(ncclGroupStart());
+  {
+    ua_status st = a2a(ctx, send, recv, 4, size_t(s.chunk()), ncclBfloat16, 2, stream);
+    if (st != UA_OK) { ncclGroupEnd(); return st; }
+    void* sd = send_delta;
+    void* rd = recv_delta;
+    st = a2a(ctx, &sd, &rd, 1, size_t(s.Nl * B * s.Hl), ncclFloat32, 4, stream);
+    if (st != UA_OK) { ncclGroupEnd(); return st; }
+  }
+  UA_NCCL(ncclGroupEnd());
+  ctx->a2a_calls += 1;
+  // 3. attention backward on the head shard [N][B][Hl][D]
+  UA_CUDA(cudaMemsetAsync(dq_acc, 0, size_t(B * s.Hl * ((N + 127) / 128 * 128) * D) * 4, stream));
+  const int64_t sn = B * int64_t(s.Hl) * D, sh = D, sb = int64_t(s.Hl) * D;
+  ua::ViewArg vdq{grad[0], sn, sh, sb}, vdk{grad[1], sn, sh, sb}, vdv{grad[2], sn, sh, sb};
+  UA_TRY(launch_attention_bwd(recv[0], recv[1], recv[2], recv[3], sn, sh, sb, vdk, vdv, dq_acc, lse, N,
+                              int64_t(s.Hl) * N, recv_delta, B * int64_t(s.Hl), 1, s.Hl, B, N, s.Hl, D, stream));
+  UA_CUDA(ua::launch_dq_finalize(dq_acc, vdq, B, N, s.Hl, D, float(1.0 / std::sqrt(double(D))), stream));
+  // 4. all-to-all #4 (fused dq, dk, dv) back to the token owners
+  void* rgrad[3] = {ws + plan.send, ws + plan.send + S, ws + plan.send + 2 * S};
+  UA_TRY(a2a(ctx, grad, rgrad, 3, size_t(s.chunk()), ncclBfloat16, 2, stream));
+  ctx->a2a_calls += 1;
+  // 5. unpack -> dq, dk, dv [B][Nl][H][D]
+  const void* usrc[3] = {rgrad[0], rgrad[1], rgrad[2]};
+  void* udst[3] = {dq, dk, dv};
+  UA_CUDA(ua::launch_unpack(usrc, udst, 3, B, s.Nl, H, D, P, stream));
+  return UA_OK;
+}
+
+ua_status ua_attn_fwd_segment(const void* q, const void* k, const void* v, float* o_seg, float* lse_seg, int64_t B,
+                              int64_t N, int Hx, int D, int64_t kv_begin, int64_t kv_end, ua_stream_t stream_) {
+  UA_TRY(ua_validate(B, N, Hx, D, 1));
+  if (!q || !k || !v || !o_seg || !lse_seg) return fail(UA_ERR_INVALID_ARG, "null tensor pointer");
+  if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o_seg) || !aligned16(lse_seg))
+    return fail(UA_ERR_INVALID_ARG, "tensor pointers must be 16-byte aligned");
+  if (kv_begin < 0 || kv_begin % 128 != 0 || kv_end <= kv_begin || kv_end > N)
+    return fail(UA_ERR_INVALID_ARG, "bad key segment [%lld, %lld) for N=%lld", (long long)kv_begin,
+                (long long)kv_end, (long long)N);
+  UA_TRY(check_device());
+  UA_TRY(check_async(nullptr));
+  const int64_t sn = int64_t(Hx) * D, sh = D, sb = N * Hx * D;
+  ua::ViewArg o{nullptr, 0, 0, 0};
+  return launch_attention_fwd(q, k, v, sn, sh, sb, o, o_seg, D, N * D, int64_t(Hx) * N * D, lse_seg, N,
+                              int64_t(Hx) * N, B, N, Hx, D, kv_begin, kv_end, reinterpret_cast<cudaStream_t>(stream_));
+}
+
+ua_status ua_lse_merge(float* o_a, float* lse_a, const float* o_b, const float* lse_b, int64_t rows, int D,
+                       ua_stream_t stream_) {
+  if (!o_a || !lse_a || !o_b || !lse_b || rows < 1 || D < 1) return fail(UA_ERR_INVALID_ARG, "bad lse_merge args");
+  UA_TRY(check_device());
+  UA_CUDA(ua::launch_lse_merge(o_a, lse_a, o_b, lse_b, rows, D, reinterpret_cast<cudaStream_t>(stream_)));
+  return UA_OK;
+}
+
+ua_status ua_f32_to_bf16_bnhd(const float* src, void* dst, int64_t B, int64_t N, int Hx, int D, ua_stream_t stream_) {
+  UA_TRY(ua_validate(B, N, Hx, D, 1));
+  if (!src || !dst || !aligned16(src) || !aligned16(dst)) return fail(UA_ERR_INVALID_ARG, "bad pointers");
+  UA_TRY(check_device());
+  ua::ViewArg v{dst, int64_t(Hx) * D, D, N * Hx * D};
+  UA_CUDA(ua::launch_f32_to_view(src, v, B, N, Hx, D, reinterpret_cast<cudaStream_t>(stream_)));
+  return UA_OK;
+}
+
+}  // extern "C"

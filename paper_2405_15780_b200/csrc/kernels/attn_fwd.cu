@@ -1,0 +1,302 @@
+// attn_fwd.cu — exact attention forward for one head shard, sm_100a.
+//
+// Computes, for every (b, h) of the launch and query row i,
+//   o_i = sum_j softmax_j(s_ij) v_j,  s_ij = q_i.k_j / sqrt(D),
+//   lse_i = ln sum_j exp(s_ij)
+// over the key range [kv_begin, kv_end): PAPER.md P:165 (§2.5, each GPU runs
+// ordinary attention over the complete sequence for its head subset) computed
+// FlashAttention-style (§2.6: tile the score matrix, never write it
+// to HBM).  With kv_begin = 0, kv_end = N it is the full attention; a strict
+// sub-range is one LSS segment merged later by lse_merge.
+//
+// Design (B200-first, not a port of any FA2/ROCm code):
+//  * one CTA = 2 query tiles of 128 rows of one (b, h); 12 warps:
+//      warp 0      TMA producer (Q once, K/V ring of kStages tiles)
+//      warp 1      tcgen05.mma issuer (single elected thread) + TMEM owner
+//      warps 4-7   softmax for query tile 0 (one row per thread)
+//      warps 8-11  softmax for query tile 1
+//  * TMEM (512 cols): S0 [0,128) S1 [128,256) O0 [256,256+D) O1 [256+D, 256+2D).
+//    S_t = Q_t K_j^T (SS MMA, M=128,N=128,K=D).  The softmax rewrites S_t in
+//    place as bf16 P_t (64 cols, packed pairs) and O_t += P_t V_j runs as a TS
+//    MMA (A = P from TMEM, B = V from smem, MN-major).  The two tiles ping-pong:
+//    while tile 0 does its softmax the tensor core runs tile 1's GEMMs.
+//  * online softmax in the log2 domain with a lazy max: the running max m used
+//    for the exponent is only raised (and O, l rescaled) when a row's max grows
+//    by more than 8 (a factor 256); the final o = O / l is exact either way
+//    because O and l carry the same stale max.
+#include "attn_common.cuh"
+#include "attn_kernels.h"
+
+namespace ua {
+
+namespace {
+
+template <int D>
+struct FwdCfg {
+  using G = TileGeom<D>;
+  static constexpr int kStages = D == 128 ? 2 : 3;
+  static constexpr int kThreads = 384;
+  static constexpr int kSmemTiles = (2 + 2 * kStages) * G::kTileBytes;
+  static constexpr int kSmemBytes = 1024 + kSmemTiles + 256;
+  static constexpr uint32_t kColS = 0;     // + t*128
+  static constexpr uint32_t kColO = 256;   // + t*D
+  static constexpr float kRescaleThreshold = 8.0f;  // log2 units
+};
+
+template <int D>
+__global__ void __launch_bounds__(384, 1) attn_fwd_kernel(const __grid_constant__ FwdParams p) {
+  using C = FwdCfg<D>;
+  using G = TileGeom<D>;
+  constexpr int kStages = C::kStages;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;                                  // [2] tiles
+  uint8_t* sK = sQ + 2 * G::kTileBytes;                // [kStages]
+  uint8_t* sV = sK + kStages * G::kTileBytes;          // [kStages]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + kStages * G::kTileBytes);
+  uint64_t* q_full = bars;
+  uint64_t* k_full = bars + 1;
+  uint64_t* v_full = k_full + kStages;
+  uint64_t* kv_empty = v_full + kStages;
+  uint64_t* s_full = kv_empty + kStages;  // [2]
+  uint64_t* p_full = s_full + 2;          // [2]
+  uint64_t* o_done = p_full + 2;          // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const int h = blockIdx.y, b = blockIdx.z;
+  const int q0 = blockIdx.x * 256;
+  const int kv_t0 = p.kv_begin / 128;
+  const int n_kv = (p.kv_end - p.kv_begin + 127) / 128;
+
+  if (threadIdx.x == 0) {
+    mbar_init(q_full, 1);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&v_full[s], 1);
+      mbar_init(&kv_empty[s], 1);
+    }
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(&s_full[t], 1);
+      mbar_init(&p_full[t], 128);
+      mbar_init(&o_done[t], 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer
+    if (elect_one()) {
+      tma_prefetch_desc(&p.tm_q);
+      tma_prefetch_desc(&p.tm_k);
+      tma_prefetch_desc(&p.tm_v);
+      mbar_arrive_expect_tx(q_full, 2 * G::kTileBytes);
+      for (int t = 0; t < 2; ++t)
+        for (int a = 0; a < G::kAtoms; ++a)
+          tma_load_4d(sQ + t * G::kTileBytes + a * G::kAtomBytes, &p.tm_q, q_full, a * G::kAtomCols,
+                      q0 + t * 128, h, b, kEvictFirst);
+      for (int j = 0; j < n_kv; ++j) {
+        const int s = j % kStages;
+        if (j >= kStages) mbar_wait(&kv_empty[s], ((j / kStages) & 1) ^ 1);
+        const int row = (kv_t0 + j) * 128;
+        mbar_arrive_expect_tx(&k_full[s], G::kTileBytes);
+        for (int a = 0; a < G::kAtoms; ++a)
+          tma_load_4d(sK + s * G::kTileBytes + a * G::kAtomBytes, &p.tm_k, &k_full[s], a * G::kAtomCols, row, h,
+                      b, kEvictLast);
+        mbar_arrive_expect_tx(&v_full[s], G::kTileBytes);
+        for (int a = 0; a < G::kAtoms; ++a)
+          tma_load_4d(sV + s * G::kTileBytes + a * G::kAtomBytes, &p.tm_v, &v_full[s], a * G::kAtomCols, row, h,
+                      b, kEvictLast);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (elect_one()) {
+      const uint32_t idesc_s = idesc_bf16_f32(128, 128, false, false);
+      const uint32_t idesc_o = idesc_bf16_f32(128, D, false, true);
+      const uint32_t sQa = smem_u32(sQ), sKa = smem_u32(sK), sVa = smem_u32(sV);
+      mbar_wait(q_full, 0);
+      tc_fence_after();
+      for (int j = 0; j <= n_kv; ++j) {
+        const int s = j % kStages;
+        if (j < n_kv) {
+          mbar_wait(&k_full[s], (j / kStages) & 1);
+          tc_fence_after();
+        }
+        for (int t = 0; t < 2; ++t) {
+          if (j > 0) {  // O_t += P_t(j-1) V_{j-1}
+            const int sp = (j - 1) % kStages;
+            mbar_wait(&p_full[t], (j - 1) & 1);
+            if (t == 0) mbar_wait(&v_full[sp], ((j - 1) / kStages) & 1);
+            tc_fence_after();
+            const uint32_t vt = sVa + sp * G::kTileBytes;
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk)
+              mma_ts(tbase + C::kColO + t * D, tbase + C::kColS + t * 128 + kk * 8, mnmajor_desc<D>(vt, kk),
+                     idesc_o, (j > 1 || kk > 0) ? 1u : 0u);
+            mma_commit(&o_done[t]);
+          }
+          if (j < n_kv) {  // S_t = Q_t K_j^T
+            const uint32_t qt = sQa + t * G::kTileBytes, kt = sKa + s * G::kTileBytes;
+#pragma unroll
+            for (int kk = 0; kk < D / 16; ++kk)
+              mma_ss(tbase + C::kColS + t * 128, kmajor_desc<D>(qt, kk), kmajor_desc<D>(kt, kk), idesc_s,
+                     kk > 0 ? 1u : 0u);
+            mma_commit(&s_full[t]);
+          }
+        }
+        if (j > 0) mma_commit(&kv_empty[(j - 1) % kStages]);
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ softmax
+    const int t = (warp - 4) / 4;
+    const int quad = warp % 4;                 // TMEM lane quadrant of this warp
+    const int row = quad * 32 + lane;          // row within the query tile
+    const int q_row = q0 + t * 128 + row;      // global query index
+    const uint32_t t_lane = tbase + (uint32_t(quad * 32) << 16);
+    const uint32_t colS = C::kColS + t * 128, colO = C::kColO + t * D;
+    const float c = p.scale_log2;
+    float m_use = -INFINITY, l = 0.f;
+
+    for (int j = 0; j < n_kv; ++j) {
+      mbar_wait(&s_full[t], j & 1);
+      tc_fence_after();
+      float sv[128];
+#pragma unroll
+      for (int cc = 0; cc < 128; cc += 32) {
+        uint32_t r[32];
+        tmem_ld32(t_lane + colS + cc, r);
+        tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) sv[cc + i] = __uint_as_float(r[i]);
+      }
+      const int kv0 = p.kv_begin + j * 128;
+      if (kv0 + 128 > p.kv_end) {
+#pragma unroll
+        for (int i = 0; i < 128; ++i)
+          if (kv0 + i >= p.kv_end) sv[i] = -INFINITY;
+      }
+      float mx[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) mx[i] = sv[i];
+#pragma unroll
+      for (int i = 8; i < 128; ++i) mx[i % 8] = fmaxf(mx[i % 8], sv[i]);
+      float rmax = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])), fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
+      const float m_new = fmaxf(m_use, rmax * c);
+      const bool need = m_new > m_use + C::kRescaleThreshold;
+      const bool warp_need = __any_sync(0xffffffffu, need);
+      const float alpha = need ? ex2(m_use - m_new) : 1.f;
+      if (need) {
+        m_use = m_new;
+        l *= alpha;
+      }
+      const float neg_m = -m_use;
+      float ls[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int cc = 0; cc < 128; cc += 32) {
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const float p0 = ex2(fmaf(sv[cc + 2 * i], c, neg_m));
+          const float p1 = ex2(fmaf(sv[cc + 2 * i + 1], c, neg_m));
+          ls[i % 4] += p0 + p1;
+          pk[i] = pack_bf16x2(p0, p1);
+        }
+        tmem_st16(t_lane + colS + cc / 2, pk);
+      }
+      l += (ls[0] + ls[1]) + (ls[2] + ls[3]);
+      // Lazy rescale of O_t.  PV_t(j-1) has completed: S_t(j), observed
+      // complete above, was issued after it by the same thread.
+      if (warp_need && j > 0) {
+        mbar_wait(&o_done[t], (j - 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int cc = 0; cc < D; cc += 32) {
+          uint32_t r[32];
+          tmem_ld32(t_lane + colO + cc, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
+          tmem_st32(t_lane + colO + cc, r);
+        }
+      }
+      tmem_st_wait();
+      tc_fence_before();
+      mbar_arrive(&p_full[t]);
+    }
+
+    // ------------------------------------------------------------ epilogue
+    mbar_wait(&o_done[t], (n_kv - 1) & 1);
+    tc_fence_after();
+    const float inv_l = 1.f / l;
+    const bool valid = q_row < p.n_q;
+    __nv_bfloat16* orow = reinterpret_cast<__nv_bfloat16*>(p.o.base) + b * p.o.sb + h * p.o.sh + int64_t(q_row) * p.o.sn;
+#pragma unroll
+    for (int cc = 0; cc < D; cc += 32) {
+      uint32_t r[32];
+      tmem_ld32(t_lane + colO + cc, r);
+      tmem_ld_wait();
+      if (p.o_f32 != nullptr) {
+        if (valid) {
+          float* frow = p.o_f32 + b * p.of_sb + h * p.of_sh + int64_t(q_row) * p.of_sn + cc;
+#pragma unroll
+          for (int i = 0; i < 32; i += 4)
+            *reinterpret_cast<float4*>(frow + i) =
+                make_float4(__uint_as_float(r[i]) * inv_l, __uint_as_float(r[i + 1]) * inv_l,
+                            __uint_as_float(r[i + 2]) * inv_l, __uint_as_float(r[i + 3]) * inv_l);
+        }
+      } else {
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          pk[i] = pack_bf16x2(__uint_as_float(r[2 * i]) * inv_l, __uint_as_float(r[2 * i + 1]) * inv_l);
+        if (valid) {
+#pragma unroll
+          for (int i = 0; i < 16; i += 4)
+            *reinterpret_cast<uint4*>(orow + cc + 2 * i) = make_uint4(pk[i], pk[i + 1], pk[i + 2], pk[i + 3]);
+        }
+      }
+    }
+    if (valid) p.lse[b * p.l_sb + h * p.l_sh + q_row] = (m_use + __log2f(l)) * kLn2;
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_free<512>(tbase);
+}
+
+template <int D>
+cudaError_t launch_fwd_impl(const FwdParams& p, int B, int Hx, cudaStream_t stream) {
+  using C = FwdCfg<D>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(attn_fwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  dim3 grid((p.n_q + 255) / 256, Hx, B);
+  attn_fwd_kernel<D><<<grid, C::kThreads, C::kSmemBytes, stream>>>(p);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_attn_fwd(const FwdParams& p, int D, int B, int Hx, cudaStream_t stream) {
+  switch (D) {
+    case 32: return launch_fwd_impl<32>(p, B, Hx, stream);
+    case 64: return launch_fwd_impl<64>(p, B, Hx, stream);
+    case 128: return launch_fwd_impl<128>(p, B, Hx, stream);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace ua

@@ -1,0 +1,74 @@
+// attn_kernels.h — internal (C++) launch interface of the CUDA kernels.  Not
+// part of the C ABI; csrc/capi.cpp is the only caller.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace ua {
+
+struct ViewArg {
+  void* base;
+  int64_t sn, sh, sb;  // element strides of token, head, batch (d contiguous)
+};
+
+struct alignas(64) FwdParams {
+  CUtensorMap tm_q;  // 4-D maps {D, N, heads, B} over the Q / K / V views
+  CUtensorMap tm_k;
+  CUtensorMap tm_v;
+  ViewArg o;          // bf16 output (used when o_f32 == nullptr)
+  float* o_f32;       // optional fp32 normalised output (LSS segments)
+  int64_t of_sn, of_sh, of_sb;
+  float* lse;         // lse[b*l_sb + h*l_sh + n]
+  int64_t l_sh, l_sb;
+  int n_q;            // number of query rows
+  int kv_begin, kv_end;  // key range; kv_begin % 128 == 0
+  float scale_log2;   // log2(e) / sqrt(D)
+};
+
+struct alignas(64) BwdParams {
+  CUtensorMap tm_q;   // {D, N, heads, B}
+  CUtensorMap tm_k;
+  CUtensorMap tm_v;
+  CUtensorMap tm_do;
+  ViewArg dk, dv;     // bf16 outputs
+  float* dq_acc;      // fp32 [B*heads][N_pad][D] accumulator, N_pad = ceil(N/128)*128 (zeroed by caller)
+  const float* lse;   // lse[b*l_sb + h*l_sh + n]
+  int64_t l_sh, l_sb;
+  const float* delta; // Delta[b*d_sb + h*d_sh + n*d_sn]
+  int64_t d_sn, d_sh, d_sb;
+  int n;              // sequence length (queries == keys)
+  int heads;
+  float scale;        // 1/sqrt(D)
+  float scale_log2;   // log2(e)/sqrt(D)
+};
+
+cudaError_t launch_attn_fwd(const FwdParams& p, int D, int B, int heads, cudaStream_t stream);
+cudaError_t launch_attn_bwd(const BwdParams& p, int D, int B, int heads, cudaStream_t stream);
+
+// ---- layout / elementwise kernels (layout.cu) --------------------------------
+// Sequence shard -> per-destination send chunks, for `ntensors` tensors:
+//   src[w]  : [B][Nl][H][D]          (rank-local sequence shard, user layout)
+//   dst[w]  : [P][Nl][B][Hl][D]      (chunk j = heads j*Hl.. of every token)
+// If delta_dst != nullptr, also Delta[b,t,h] = sum_d dO.O in fp32 from
+// (dout, out) [B][Nl][H][D] into delta_dst [P][Nl][B][Hl] (P == 1: [B][H][Nl]).
+cudaError_t launch_pack(const void* const* src, void* const* dst, int ntensors, int64_t B, int64_t Nl, int H, int D,
+                        int P, const void* dout, const void* out, float* delta_dst, cudaStream_t stream);
+// Received head chunks -> sequence shard, for `ntensors` tensors:
+//   src[w]  : [P][Nl][B][Hl][D]      (chunk s = source rank s)
+//   dst[w]  : [B][Nl][H][D]
+cudaError_t launch_unpack(const void* const* src, void* const* dst, int ntensors, int64_t B, int64_t Nl, int H,
+                          int D, int P, cudaStream_t stream);
+// dq = bf16(scale * dq_acc), dq_acc [B*heads][N_pad][D] fp32 (N_pad = N rounded up to 128) -> view
+cudaError_t launch_dq_finalize(const float* dq_acc, ViewArg dq, int64_t B, int64_t N, int heads, int D, float scale,
+                               cudaStream_t stream);
+// Exact merge of two LSS segment results (in place into a):
+//   lse = logaddexp(lse_a, lse_b); O = e^{lse_a-lse} O_a + e^{lse_b-lse} O_b
+cudaError_t launch_lse_merge(float* o_a, float* lse_a, const float* o_b, const float* lse_b, int64_t rows, int D,
+                             cudaStream_t stream);
+// fp32 [rows][D] -> bf16 view rows (row r = (b, h, n) of [B][heads][N])
+cudaError_t launch_f32_to_view(const float* src, ViewArg dst, int64_t B, int64_t N, int heads, int D,
+                               cudaStream_t stream);
+
+}  // namespace ua

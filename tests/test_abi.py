@@ -1,0 +1,97 @@
+"""Host-only checks of the C-ABI library: it loads, exports every symbol
+include/ulysses_attn.h declares, validates shapes with the documented status
+codes, plans workspaces, and fails loudly (no CPU fallback) without a GPU."""
+import os
+import re
+
+import pytest
+import torch
+
+import paper_2405_15780_b200 as ua
+from paper_2405_15780_b200 import build as ua_build
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "ulysses_attn.h")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def built():
+    ua_build.build()
+
+
+def declared_functions():
+    text = open(HEADER).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(ua_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_header_declares_exports():
+    assert declared_functions() == sorted(ua.EXPORTS)
+
+
+def test_library_exports_every_declared_symbol():
+    L = ua.lib()
+    for name in declared_functions():
+        assert hasattr(L, name), name
+    # and nm agrees (extern "C", unmangled, defined)
+    import subprocess
+    syms = subprocess.run(["nm", "-D", "--defined-only", ua.LIB_PATH], capture_output=True, text=True).stdout
+    for name in declared_functions():
+        assert re.search(rf"\bT {name}$", syms, flags=re.M), name
+
+
+def test_version_and_status_strings():
+    assert "sm_100a" in ua.version()
+    for code, name in ua.STATUS.items():
+        assert ua.lib().ua_status_string(code).decode() == name
+
+
+@pytest.mark.parametrize("args,status", [
+    ((1, 16, 4, 64, 8), 2),      # H=4, P=8 -> HeadDivisibility
+    ((1, 12, 6, 64, 4), 2),      # P does not divide H
+    ((1, 10, 4, 64, 4), 3),      # N % P != 0 -> SeqDivisibility
+    ((1, 16, 4, 72, 2), 4),      # D=72 unsupported (Table 1 ViT-10B: NEXT)
+    ((0, 16, 4, 64, 1), 1),
+    ((1, 0, 4, 64, 1), 1),
+    ((1, 1 << 31, 32, 64, 8), 4),
+    ((1, 256, 4, 32, 1), 0),     # c1
+    ((1, 188416, 32, 64, 8), 0),  # c4 at P=8
+    ((1, 1048576, 32, 128, 8), 0),  # c5
+])
+def test_validate_codes(args, status):
+    assert ua.lib().ua_validate(*args) == status
+    if status:
+        assert ua.lib().ua_last_error().decode() != ""
+
+
+def test_python_errors():
+    with pytest.raises(ua.HeadDivisibilityError):
+        ua.validate(1, 16, 4, 64, 8)
+    with pytest.raises(ua.SeqDivisibilityError):
+        ua.validate(1, 10, 4, 64, 4)
+
+
+def test_workspace_plan():
+    B, N, H, D = 1, 188416, 32, 64
+    shard = B * N * H * D * 2
+    f1, b1 = ua.workspace_size(B, N, H, D, 1)
+    assert f1 == 0 and b1 >= B * N * H * 4 + B * N * H * D * 4
+    for P in (2, 4, 8):
+        f, b = ua.workspace_size(B, N, H, D, P)
+        s = shard // P
+        assert 7 * s <= f <= 7 * s + 4096
+        assert b >= 11 * s + 2 * s + 2 * B * (N // P) * H * 4
+
+
+def test_no_cpu_fallback():
+    """Without a CUDA device every compute entry point fails loudly."""
+    if torch.cuda.is_available():
+        pytest.skip("has a GPU")
+    import ctypes
+    h = ctypes.c_void_p(0)
+    st = ua.lib().ua_ctx_create(None, 1, 0, 0, ctypes.byref(h))
+    assert st in (4, 5) and not h.value
+    st = ua.lib().ua_attn_fwd_segment(*(ctypes.c_void_p(16),) * 5, 1, 256, 4, 64, 0, 256, None)
+    assert st in (4, 5)
+    with pytest.raises(ValueError):
+        ua.ulysses_attn_fwd(None, torch.zeros(1, 4, 1, 64), torch.zeros(1, 4, 1, 64), torch.zeros(1, 4, 1, 64))

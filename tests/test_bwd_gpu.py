@@ -1,0 +1,104 @@
+"""GPU parity of the Ulysses backward at P=1 against the fp64 oracle, through
+the C ABI (dq, dk, dv for the loss <out, dout>).  Inputs from synth only."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from tests.parity import gate_grad
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ua():
+    import paper_2405_15780_b200 as m
+    from paper_2405_15780_b200 import build
+    build.build()
+    return m
+
+
+@pytest.fixture(scope="module")
+def ctx(ua):
+    c = ua.Context(P=1)
+    yield c
+    c.close()
+
+
+def run_fwd_bwd(ua, ctx, q, k, v, do):
+    qc, kc, vc, dc = (t.cuda() for t in (q, k, v, do))
+    r = ua.ulysses_attn_fwd(ctx, qc, kc, vc)
+    dq, dk, dv = ua.ulysses_attn_bwd(ctx, qc, kc, vc, r.out, r.lse, dc)
+    torch.cuda.synchronize()
+    return tuple(t.float().cpu().numpy() for t in (dq, dk, dv))
+
+
+def check(ua, ctx, B, N, H, D, sigma, seed):
+    q, k, v, do = synth.qkv(B, N, H, D, seed=seed, sigma_qk=sigma, with_do=True)
+    got = run_fwd_bwd(ua, ctx, q, k, v, do)
+    dq, dk, dv, _, _, gabs = oracle.attn_bwd(*(synth.to_f64(t) for t in (q, k, v, do)), with_abs=True)
+    stats = {}
+    for name, g, ref, a in zip(("dq", "dk", "dv"), got, (dq, dk, dv), gabs):
+        stats[name] = gate_grad(g, ref, gate_a=sigma == 1.0, gabs=a)
+    return stats
+
+
+@pytest.mark.parametrize("N,H,D,sigma", [
+    (256, 4, 32, 1.0),      # c1
+    (256, 4, 32, 2.0),
+    (1, 2, 64, 1.0),        # one token: dV = dO, dQ = dK = 0
+    (127, 2, 64, 1.0),
+    (129, 2, 64, 2.0),
+    (384, 2, 64, 1.0),
+    (640, 2, 128, 1.0),
+    (1000, 2, 128, 2.0),
+    (4050, 2, 64, 1.0),     # P:263 seq 4050 (ragged tail)
+    (2048, 2, 32, 2.0),
+])
+def test_bwd_parity_small(ua, ctx, N, H, D, sigma):
+    check(ua, ctx, 1, N, H, D, sigma, seed=100 + N)
+
+
+def test_bwd_batch2(ua, ctx):
+    check(ua, ctx, 2, 384, 2, 64, 1.0, seed=5)
+
+
+@pytest.mark.parametrize("sigma", [1.0, 2.0])
+def test_bwd_parity_c2(ua, ctx, sigma):
+    """c2: N=8192, H=16, D=64, full oracle backward on 4 of the 16 heads
+    (heads are independent; the GPU runs all 16)."""
+    B, N, H, D = 1, 8192, 16, 64
+    q, k, v, do = synth.qkv(B, N, H, D, seed=synth.BASE_SEED, sigma_qk=sigma, with_do=True)
+    got = run_fwd_bwd(ua, ctx, q, k, v, do)
+    heads = [0, 5, 10, 15]
+    sub = [synth.to_f64(t)[:, :, heads] for t in (q, k, v, do)]
+    dq, dk, dv, _, _, gabs = oracle.attn_bwd(*sub, with_abs=True)
+    for g, ref, a in zip(got, (dq, dk, dv), gabs):
+        gate_grad(g[:, :, heads], ref, gate_a=sigma == 1.0, gabs=a)
+
+
+def test_bwd_invariants(ua, ctx):
+    """Exact-math invariants on the GPU gradients (oracle-free): sum_j dK_j = 0,
+    sum_j dV_j = sum_i dO_i, <Q,dQ> = <K,dK> per head; constant V -> dQ = dK = 0."""
+    N, H, D = 2048, 4, 64
+    q, k, v, do = synth.qkv(1, N, H, D, seed=9, with_do=True)
+    dq, dk, dv = run_fwd_bwd(ua, ctx, q, k, v, do)
+    qf, kf, dof = (synth.to_f64(t) for t in (q, k, do))
+    scale_k = np.abs(dk).sum(axis=1)
+    assert np.all(np.abs(dk.sum(axis=1)) <= 2e-2 * scale_k + 1e-3)
+    assert np.all(np.abs(dv.sum(axis=1) - dof.sum(axis=1)) <= 1e-2 * np.abs(dv).sum(axis=1) + 1e-2)
+    lhs = np.einsum("bnhd,bnhd->h", qf, dq)
+    rhs = np.einsum("bnhd,bnhd->h", kf, dk)
+    assert np.all(np.abs(lhs - rhs) <= 2e-2 * (np.abs(lhs) + np.abs(rhs)) + 1.0)
+    vc = torch.broadcast_to(v[:, :1], v.shape).contiguous()
+    dq0, dk0, _ = run_fwd_bwd(ua, ctx, q, k, vc, do)
+    assert np.abs(dq0).max() < 2e-2 and np.abs(dk0).max() < 2e-2
+
+
+def test_bwd_deterministic_dkdv(ua, ctx):
+    """dK, dV are computed without atomics: bitwise reproducible."""
+    q, k, v, do = synth.qkv(1, 1024, 2, 64, seed=13, with_do=True)
+    a = run_fwd_bwd(ua, ctx, q, k, v, do)
+    b = run_fwd_bwd(ua, ctx, q, k, v, do)
+    assert np.array_equal(a[1], b[1]) and np.array_equal(a[2], b[2])

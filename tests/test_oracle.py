@@ -41,6 +41,17 @@ def test_fwd_matches_torch_sdpa_fp64(B, N, H, D):
     assert np.abs(lse - torch.logsumexp(s, dim=-1).numpy()).max() < 1e-12
 
 
+def test_fwd_abs_helper():
+    """absv = sum_j P_ij |v_jd|: equals out for V >= 0 and out(|V|) always."""
+    q, k, v = rnd((1, 40, 2, 8), 23), rnd((1, 40, 2, 8), 24), rnd((1, 40, 2, 8), 25)
+    out, lse, absv = oracle.attn_fwd(q, k, v, with_abs=True)
+    out2, lse2 = oracle.attn_fwd(q, k, v)
+    assert np.array_equal(out, out2) and np.array_equal(lse, lse2)
+    o_abs, _ = oracle.attn_fwd(q, k, np.abs(v))
+    assert np.abs(absv - o_abs).max() < 1e-14
+    assert np.all(absv >= np.abs(out) - 1e-14)
+
+
 def test_fwd_cross_attention_shapes():
     """Nq != Nk (used by the segment tests) against torch SDPA."""
     q, k, v = rnd((1, 9, 2, 8), 4), rnd((1, 21, 2, 8), 5), rnd((1, 21, 2, 8), 6)
@@ -285,3 +296,27 @@ def test_lss_merge_weights_are_segment_mass():
     _, lse = lss.merge(parts)
     mass = sum(np.exp(l - lse) for _, l in parts)
     assert np.abs(mass - 1).max() < 1e-14
+
+
+def test_bwd_abs_helpers():
+    """gabs = (scale (|dS|+E)|K|, scale (|dS|+E)^T|Q|, P^T|dO|): the third equals dV
+    computed with |dO| (dV is linear in dO); all bound |grad| from above; the
+    first two against materialised numpy on a tiny case."""
+    N, H, D = 23, 2, 8
+    q, k, v, do = (rnd((1, N, H, D), s) for s in (100, 101, 102, 103))
+    dq, dk, dv, out, lse, (aq, ak, av) = oracle.attn_bwd(q, k, v, do, with_abs=True)
+    _, _, dv_abs, _, _ = oracle.attn_bwd(q, k, v, np.abs(do))
+    assert np.abs(av - dv_abs).max() < 1e-13
+    for g, a in ((dq, aq), (dk, ak), (dv, av)):
+        assert np.all(a >= np.abs(g) - 1e-13)
+    sc = 1 / math.sqrt(D)
+    for h in range(H):
+        S = q[0, :, h] @ k[0, :, h].T * sc
+        P = np.exp(S - S.max(1, keepdims=True))
+        P /= P.sum(1, keepdims=True)
+        dP = do[0, :, h] @ v[0, :, h].T
+        O = P @ v[0, :, h]
+        dS = P * (dP - (do[0, :, h] * O).sum(1, keepdims=True))
+        E = P * np.abs(do[0, :, h] * O).sum(1, keepdims=True)
+        assert np.abs(aq[0, :, h] - sc * (np.abs(dS) + E) @ np.abs(k[0, :, h])).max() < 1e-12
+        assert np.abs(ak[0, :, h] - sc * (np.abs(dS) + E).T @ np.abs(q[0, :, h])).max() < 1e-12
