@@ -1,0 +1,336 @@
+#!/usr/bin/env python3
+"""Benchmark of the Ulysses sequence-parallel exact-attention hot path on B200.
+
+One step = the whole hot path of SURVEY.md §8(a) on one batch: the Ulysses
+forward (pack -> a2a -> attention -> a2a -> unpack) and backward (pack + Delta
+-> a2a -> attention backward -> dQ finalize -> a2a -> unpack) of one attention
+layer at BASELINE.json's headline workload c4: N = 188,416 tokens (the paper's
+188K full-attention climate run), H = 32, D = 64, batch 1, bf16, with
+the sequence split over the N GPUs (P = --gpus).  The work is fixed as GPUs
+are added (strong scaling).
+
+    python bench.py [--gpus N --steps K --warmup W]
+    torchrun --nproc-per-node N bench.py --gpus N ...      (N > 1)
+    python bench.py --impl reference                        (fp64 CPU oracle arm)
+
+Rank 0 prints one JSON line.  value = aggregate attention TFLOP/s (fwd 4*N^2*H*D
++ bwd 10*N^2*H*D per step, FlashAttention accounting, no causal halving) over
+the max-over-ranks device time; tokens/s and % of the measured bf16 peak ride
+along.  Inputs are resident in HBM for `value`; `e2e` repeats the measurement
+through the public API with pinned-host inputs copied in and results copied out
+every step.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import torch
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "attention TFLOPS & tokens/s at 188K tokens, 1/2/4/8 B200 (% of BF16 peak)"
+UNIT = "TFLOP/s"
+WORKLOAD = dict(name="c4", B=1, N=188416, H=32, D=64)
+
+
+def flops_per_step(B, N, H, D):
+    fwd = 4.0 * B * N * N * H * D
+    return fwd, 2.5 * fwd
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return dict(bf16_burst=d["bf16_tflops"], bf16_sustained=d.get("bf16_tflops_sustained", d["bf16_tflops"]),
+                    hbm_gbs=d["hbm_gbs"], source="MEASURED_PEAKS.json (measured)")
+    return dict(bf16_burst=1590.0, bf16_sustained=1400.0, hbm_gbs=6650.0,
+                source="B200_PROFILING.md fallback")
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, enabled=True):
+        self.proc = None
+        self.enabled = enabled
+
+    def __enter__(self):
+        if self.enabled:
+            try:
+                self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                              "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                                             text=True)
+            except Exception:
+                self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.rows = []
+        if self.proc is None:
+            return
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out = ""
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) >= 9:
+                self.rows.append(f)
+
+    def summary(self, devices):
+        rows = [r for r in getattr(self, "rows", []) if r[0].isdigit() and int(r[0]) in devices]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": float(rows[0][2]),
+                "reasons": reasons, "samples": len(rows),
+                "power_w_max": max(float(r[3]) for r in rows if r[3].replace(".", "").isdigit())}
+
+
+def cpu_baseline(steps=1, n_sample=24576, D=64):
+    """The fp64 oracle as it stands: fwd + bwd of one head over the first
+    n_sample tokens (same D), timed on this host's cores."""
+    import numpy as np
+    import oracle
+    import synth
+    q, k, v, do = synth.qkv(1, n_sample, 1, D, seed=synth.BASE_SEED, with_do=True)
+    args = [synth.to_f64(t) for t in (q, k, v, do)]
+    oracle.num_threads()
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        oracle.attn_fwd(*args[:3])
+        oracle.attn_bwd(*args)
+        times.append(time.perf_counter() - t0)
+    fwd, bwd = flops_per_step(1, n_sample, 1, D)
+    t = float(np.mean(times))
+    return dict(value=(fwd + bwd) / t / 1e12, unit=UNIT, cores=oracle.num_threads(), kind="oracle",
+                sample=f"fwd+bwd of 1 of {WORKLOAD['H']} heads over the first {n_sample} of {WORKLOAD['N']} tokens "
+                       f"(D={D}), fp64 oracle, {steps} run(s) of {t:.2f} s; algorithmic flops 14*n^2*D per head",
+                seconds=t)
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    n_sample = 8192
+    W, K = args.warmup, args.steps
+    base = cpu_baseline(steps=1, n_sample=n_sample)  # warm-up compile / first touch
+    for _ in range(max(0, W - 1)):
+        cpu_baseline(steps=1, n_sample=n_sample)
+    r = cpu_baseline(steps=K, n_sample=n_sample)
+    out = {"impl": "reference", "metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": args.gpus,
+           "steps": K, "warmup": W, "ms_per_step": r["seconds"] * 1e3, "higher_is_better": True,
+           "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": "c4 (sampled): fwd+bwd of one head, first 8192 of 188416 tokens, D=64",
+                      "B": 1, "N": WORKLOAD["N"], "H": WORKLOAD["H"], "D": WORKLOAD["D"]},
+           "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")},
+           "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    del base
+    print(json.dumps(out), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--N", type=int, default=WORKLOAD["N"])
+    ap.add_argument("--H", type=int, default=WORKLOAD["H"])
+    ap.add_argument("--D", type=int, default=WORKLOAD["D"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import paper_2405_15780_b200 as ua
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    P = world
+    if args.gpus != world:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}; using {world}", file=sys.stderr)
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    B, N, H, D = WORKLOAD["B"], args.N, args.H, args.D
+    ua.validate(B, N, H, D, P)
+    Nl = N // P
+    ctx = ua.Context(P=P, rank=rank, device=local)
+    dev = torch.device("cuda", local)
+    g = torch.Generator(device=dev).manual_seed(1234 + rank)
+    shape = (B, Nl, H, D)
+    q, k, v, do = (torch.randn(shape, device=dev, generator=g, dtype=torch.float32).to(torch.bfloat16)
+                   for _ in range(4))
+    fb, bb = ua.workspace_size(B, N, H, D, P)
+    ctx.workspace(max(fb, bb))
+    out = torch.empty_like(q)
+    lse = torch.empty((B, H // P, N), dtype=torch.float32, device=dev)
+    dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+    stream = torch.cuda.current_stream()
+
+    def step(qq=q, kk=k, vv=v, dd=do):
+        ua.ulysses_attn_fwd(ctx, qq, kk, vv, out=out, lse=lse)
+        ua.ulysses_attn_bwd(ctx, qq, kk, vv, out, lse, dd, dq=dq, dk=dk, dv=dv)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    ctx.phase_times()  # drop warm-up records
+    calls0, bytes0 = ctx.comm_stats()
+
+    # ---------------------------------------------------------------- timed
+    ctx.enable_timing(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(enabled=(rank == 0)) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    ms_total = max_over_ranks(e0.elapsed_time(e1))
+    ctx.enable_timing(False)
+    phases = ctx.phase_times()
+    calls1, bytes1 = ctx.comm_stats()
+    ms_step = ms_total / args.steps
+
+    fwd_f, bwd_f = flops_per_step(B, N, H, D)
+    tflops = (fwd_f + bwd_f) / (ms_step * 1e-3) / 1e12
+    peaks = load_peaks()
+
+    # roofline of the dominant kernel (attention backward), per launch on this rank
+    def kstats(name, flops_total):
+        ms, n = phases[name]
+        if n == 0:
+            return None
+        avg = ms / n
+        fl = flops_total / P  # this rank's heads
+        return dict(avg_ms=avg, launches=n, tflops=fl / (avg * 1e-3) / 1e12)
+
+    kb = kstats("attn_bwd", bwd_f)
+    kf = kstats("attn_fwd", fwd_f)
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get(f"attn_bwd_D{D}_N{N}_P{P}")
+        except Exception:
+            traffic = None
+    roofline = {"bound": "tensor", "kernel": "attn_bwd_kernel", "achieved": kb["tflops"],
+                "peak": peaks["bf16_sustained"], "unit": UNIT, "frac": kb["tflops"] / peaks["bf16_sustained"],
+                "frac_of_burst": kb["tflops"] / peaks["bf16_burst"], "peak_source": peaks["source"] + " sustained",
+                "traffic": traffic,
+                "flops_per_launch": bwd_f / P, "flops_formula": "10*B*N^2*(H/P)*D per launch (5 GEMMs incl. recompute)"}
+    fwd_roof = {"kernel": "attn_fwd_kernel", "achieved": kf["tflops"], "frac": kf["tflops"] / peaks["bf16_sustained"],
+                "avg_ms": kf["avg_ms"]}
+    launches = sum(n for name, (ms, n) in phases.items() if not name.startswith("a2a"))
+    phase_ms = {name: ms / args.steps for name, (ms, n) in phases.items() if n}
+    a2a_ms = sum(ms for name, (ms, n) in phases.items() if name.startswith("a2a"))
+    a2a_bytes = bytes1 - bytes0
+
+    # ---------------------------------------------------------------- e2e
+    e2e = None
+    if not args.no_e2e:
+        hq, hk, hv, hd = (t.cpu().pin_memory() for t in (q, k, v, do))
+        ho, hdq, hdk, hdv = (torch.empty(shape, dtype=torch.bfloat16).pin_memory() for _ in range(4))
+        dq_, dk_, dv_, do_ = (torch.empty_like(q) for _ in range(4))
+
+        def e2e_step():
+            q_ = hq.to(dev, non_blocking=True)
+            k_ = hk.to(dev, non_blocking=True)
+            v_ = hv.to(dev, non_blocking=True)
+            d_ = hd.to(dev, non_blocking=True)
+            r = ua.ulysses_attn_fwd(ctx, q_, k_, v_, out=out, lse=lse)
+            ua.ulysses_attn_bwd(ctx, q_, k_, v_, r.out, r.lse, d_, dq=dq, dk=dk, dv=dv)
+            ho.copy_(out, non_blocking=True)
+            hdq.copy_(dq, non_blocking=True)
+            hdk.copy_(dk, non_blocking=True)
+            hdv.copy_(dv, non_blocking=True)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(args.steps):
+            e2e_step()
+        b.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        ms_e2e = max_over_ranks(a.elapsed_time(b)) / args.steps
+        nbytes = q.numel() * 2
+        e2e = {"value": (fwd_f + bwd_f) / (ms_e2e * 1e-3) / 1e12, "unit": UNIT, "ms_per_step": ms_e2e,
+               "h2d_bytes_per_step": 4 * nbytes, "d2h_bytes_per_step": 4 * nbytes,
+               "tokens_per_s": B * N / (ms_e2e * 1e-3),
+               "path": "pinned host q,k,v,dO -> H2D -> ua_ulysses_attn_fwd/bwd -> D2H out,dq,dk,dv (per rank)"}
+
+    if rank == 0:
+        res = {
+            "metric": METRIC, "value": tflops, "unit": UNIT, "n_gpus": P, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": f"c4: Ulysses attention fwd+bwd, N={N} tokens, H={H}, D={D}, B={B}, P={P}",
+                       "B": B, "N": N, "H": H, "D": D, "P": P, "parallelism": f"ulysses-sp{P}",
+                       "l2": "inputs larger than L2 (each q/k/v/dO shard "
+                             f"{q.numel() * 2 / 1e6:.0f} MB; working set > 126 MB)",
+                       "inputs": "N(0,1) bf16, torch.randn seeded per rank"},
+            "tokens_per_s": B * N / (ms_step * 1e-3),
+            "pct_of_bf16_peak": tflops / (P * peaks["bf16_sustained"]) * 100,
+            "pct_of_bf16_burst_peak": tflops / (P * peaks["bf16_burst"]) * 100,
+            "fwd_tflops_per_gpu_kernel": kf["tflops"], "bwd_tflops_per_gpu_kernel": kb["tflops"],
+            "roofline": roofline, "roofline_fwd": fwd_roof,
+            "phases_ms_per_step": phase_ms,
+            "a2a": {"calls": calls1 - calls0, "bytes_sent_per_rank": a2a_bytes,
+                    "GBps": (a2a_bytes / (a2a_ms * 1e-3) / 1e9) if a2a_ms > 0 else None},
+            "gpu_launches": launches,
+            "clocks": clk.summary(set(range(torch.cuda.device_count()))),
+            "e2e": e2e,
+        }
+        if P == 1 and not args.no_cpu_baseline:
+            cb = cpu_baseline(steps=1)
+            res["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        print(json.dumps(res), flush=True)
+    ctx.close()
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -88,6 +88,29 @@ ua_status ua_ctx_destroy(ua_ctx* ctx);
  * rank sent to OTHER ranks. Either pointer may be NULL. */
 ua_status ua_ctx_comm_stats(const ua_ctx* ctx, int64_t* a2a_calls, int64_t* a2a_bytes_sent);
 
+/* Per-phase device timing (for benchmarks; off by default).  When enabled,
+ * every fwd / bwd call records a CUDA event pair around each phase on the
+ * call's stream.  ua_ctx_phase_times synchronises those events, ADDS the
+ * elapsed milliseconds of each phase since the last query into ms[phase] and
+ * launches[phase] (arrays of UA_NUM_PHASES, either may be NULL), and resets.
+ * Phases: */
+enum {
+  UA_PHASE_PACK_FWD = 0,   /* sequence shard -> head chunks (q, k, v)      */
+  UA_PHASE_A2A_FWD_IN,     /* all-to-all #1                                */
+  UA_PHASE_ATTN_FWD,       /* attention forward kernel                     */
+  UA_PHASE_A2A_FWD_OUT,    /* all-to-all #2                                */
+  UA_PHASE_UNPACK_FWD,     /* head chunks -> out                           */
+  UA_PHASE_PACK_BWD,       /* q, k, v, dO pack + Delta                     */
+  UA_PHASE_A2A_BWD_IN,     /* all-to-all #3                                */
+  UA_PHASE_ATTN_BWD,       /* attention backward kernel (+ dQ zeroing)     */
+  UA_PHASE_DQ_FINALIZE,    /* fp32 dQ -> bf16                              */
+  UA_PHASE_A2A_BWD_OUT,    /* all-to-all #4                                */
+  UA_PHASE_UNPACK_BWD,     /* head chunks -> dq, dk, dv                    */
+  UA_NUM_PHASES
+};
+ua_status ua_ctx_enable_timing(ua_ctx* ctx, int enable);
+ua_status ua_ctx_phase_times(ua_ctx* ctx, double* ms, int64_t* launches);
+
 /* ------------------------------------------------------------- forward
  * q, k, v : bf16 [B][N/P][H][D]   this rank's sequence shard (inputs)
  * out     : bf16 [B][N/P][H][D]   attention output, same shard (written)

@@ -28,8 +28,12 @@ STATUS = {0: "UA_OK", 1: "UA_ERR_INVALID_ARG", 2: "UA_ERR_HEAD_DIVISIBILITY", 3:
 # Every symbol include/ulysses_attn.h declares.
 EXPORTS = ("ua_version", "ua_status_string", "ua_last_error", "ua_validate", "ua_workspace_size",
            "ua_get_unique_id", "ua_ctx_create", "ua_ctx_destroy", "ua_ctx_comm_stats",
+           "ua_ctx_enable_timing", "ua_ctx_phase_times",
            "ua_ulysses_attn_fwd", "ua_ulysses_attn_bwd", "ua_attn_fwd_segment", "ua_lse_merge",
            "ua_f32_to_bf16_bnhd")
+
+PHASES = ("pack_fwd", "a2a_fwd_in", "attn_fwd", "a2a_fwd_out", "unpack_fwd", "pack_bwd", "a2a_bwd_in",
+          "attn_bwd", "dq_finalize", "a2a_bwd_out", "unpack_bwd")
 
 
 class UlyssesError(RuntimeError):
@@ -68,6 +72,8 @@ def lib():
         L.ua_ctx_create.argtypes = [ctypes.c_char_p, i32, i32, i32, ctypes.POINTER(vp)]
         L.ua_ctx_destroy.argtypes = [vp]
         L.ua_ctx_comm_stats.argtypes = [vp, ctypes.POINTER(i64), ctypes.POINTER(i64)]
+        L.ua_ctx_enable_timing.argtypes = [vp, i32]
+        L.ua_ctx_phase_times.argtypes = [vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i64)]
         L.ua_ulysses_attn_fwd.argtypes = [vp, vp, vp, vp, vp, vp, i64, i64, i32, i32, i32, vp, sz, vp]
         L.ua_ulysses_attn_bwd.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, i64, i64, i32, i32, i32, vp, sz, vp]
         L.ua_attn_fwd_segment.argtypes = [vp, vp, vp, vp, vp, i64, i64, i32, i32, i64, i64, vp]
@@ -162,6 +168,17 @@ class Context:
         c, b = ctypes.c_int64(0), ctypes.c_int64(0)
         _check(lib().ua_ctx_comm_stats(self._h, ctypes.byref(c), ctypes.byref(b)))
         return c.value, b.value
+
+    def enable_timing(self, on: bool = True):
+        _check(lib().ua_ctx_enable_timing(self._h, 1 if on else 0))
+
+    def phase_times(self) -> dict:
+        """{phase: (ms summed since last query, launches)}; synchronises."""
+        n = len(PHASES)
+        ms = (ctypes.c_double * n)()
+        cnt = (ctypes.c_int64 * n)()
+        _check(lib().ua_ctx_phase_times(self._h, ms, cnt))
+        return {PHASES[i]: (ms[i], cnt[i]) for i in range(n)}
 
     def workspace(self, nbytes: int) -> torch.Tensor:
         """Cached device workspace of at least nbytes."""

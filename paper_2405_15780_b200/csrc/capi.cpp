@@ -12,6 +12,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "kernels/attn_kernels.h"
 #include "tma_host.h"
@@ -23,7 +24,48 @@ struct ua_ctx {
   ncclComm_t comm = nullptr;
   int64_t a2a_calls = 0;
   int64_t a2a_bytes = 0;
+  // phase timing
+  bool timing = false;
+  struct Rec {
+    int phase;
+    cudaEvent_t a, b;
+  };
+  std::vector<Rec> pending;
+  std::vector<cudaEvent_t> pool;
+  cudaEvent_t get_event() {
+    if (!pool.empty()) {
+      cudaEvent_t e = pool.back();
+      pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+  }
 };
+
+namespace {
+// RAII phase marker: records an event pair around a phase when timing is on.
+struct Phase {
+  ua_ctx* ctx;
+  cudaStream_t stream;
+  ua_ctx::Rec rec{};
+  Phase(ua_ctx* c, int phase, cudaStream_t s) : ctx(c), stream(s) {
+    if (ctx && ctx->timing) {
+      rec.phase = phase;
+      rec.a = ctx->get_event();
+      rec.b = ctx->get_event();
+      cudaEventRecord(rec.a, stream);
+    }
+  }
+  ~Phase() {
+    if (ctx && ctx->timing) {
+      cudaEventRecord(rec.b, stream);
+      ctx->pending.push_back(rec);
+    }
+  }
+};
+}  // namespace
 
 namespace {
 
@@ -308,6 +350,11 @@ ua_status ua_ctx_destroy(ua_ctx* ctx) {
   if (!ctx) return UA_OK;
   ncclResult_t r = ncclSuccess;
   if (ctx->comm) r = ncclCommDestroy(ctx->comm);
+  for (auto& rec : ctx->pending) {
+    cudaEventDestroy(rec.a);
+    cudaEventDestroy(rec.b);
+  }
+  for (cudaEvent_t e : ctx->pool) cudaEventDestroy(e);
   delete ctx;
   if (r != ncclSuccess) return fail(UA_ERR_NCCL, "ncclCommDestroy: %s", ncclGetErrorString(r));
   return UA_OK;
@@ -340,6 +387,7 @@ ua_status ua_ulysses_attn_fwd(ua_ctx* ctx, const void* q, const void* k, const v
   if (P == 1) {
     const int64_t sn = int64_t(H) * D, sh = D, sb = N * H * D;
     ua::ViewArg o{out, sn, sh, sb};
+    Phase ph(ctx, UA_PHASE_ATTN_FWD, stream);
     return launch_attention_fwd(q, k, v, sn, sh, sb, o, nullptr, 0, 0, 0, lse, N, int64_t(H) * N, B, N, H, D, 0, N,
                                 stream);
   }
@@ -349,25 +397,36 @@ ua_status ua_ulysses_attn_fwd(ua_ctx* ctx, const void* q, const void* k, const v
   void* send[3] = {ws + plan.send, ws + plan.send + S, ws + plan.send + 2 * S};
   void* recv[3] = {ws + plan.recv, ws + plan.recv + S, ws + plan.recv + 2 * S};
   const void* src[3] = {q, k, v};
-  // 1. pack (sequence shard -> per-destination head chunks)
-  UA_CUDA(ua::launch_pack(src, send, 3, B, s.Nl, H, D, P, nullptr, nullptr, nullptr, stream));
-  // 2. all-to-all #1 (fused q, k, v): rank j receives all N tokens of its head block
-  UA_TRY(a2a(ctx, send, recv, 3, size_t(s.chunk()), ncclBfloat16, 2, stream));
-  ctx->a2a_calls += 1;
+  {  // 1. pack (sequence shard -> per-destination head chunks)
+    Phase ph(ctx, UA_PHASE_PACK_FWD, stream);
+    UA_CUDA(ua::launch_pack(src, send, 3, B, s.Nl, H, D, P, nullptr, nullptr, nullptr, stream));
+  }
+  {  // 2. all-to-all #1 (fused q, k, v): rank j receives all N tokens of its head block
+    Phase ph(ctx, UA_PHASE_A2A_FWD_IN, stream);
+    UA_TRY(a2a(ctx, send, recv, 3, size_t(s.chunk()), ncclBfloat16, 2, stream));
+    ctx->a2a_calls += 1;
+  }
   // 3. attention on the head shard, layout [N][B][Hl][D]; O straight into the send layout of #2
   const int64_t sn = B * int64_t(s.Hl) * D, sh = D, sb = int64_t(s.Hl) * D;
   void* o_head = ws + plan.o_head;
   ua::ViewArg o{o_head, sn, sh, sb};
-  UA_TRY(launch_attention_fwd(recv[0], recv[1], recv[2], sn, sh, sb, o, nullptr, 0, 0, 0, lse, N, int64_t(s.Hl) * N, B,
-                              N, s.Hl, D, 0, N, stream));
-  // 4. all-to-all #2: token block i of every local head goes back to rank i
+  {
+    Phase ph(ctx, UA_PHASE_ATTN_FWD, stream);
+    UA_TRY(launch_attention_fwd(recv[0], recv[1], recv[2], sn, sh, sb, o, nullptr, 0, 0, 0, lse, N,
+                                int64_t(s.Hl) * N, B, N, s.Hl, D, 0, N, stream));
+  }
   void* recv_o = ws + plan.send;
-  UA_TRY(a2a(ctx, &o_head, &recv_o, 1, size_t(s.chunk()), ncclBfloat16, 2, stream));
-  ctx->a2a_calls += 1;
-  // 5. unpack head chunks -> [B][Nl][H][D]
-  const void* usrc[1] = {recv_o};
-  void* udst[1] = {out};
-  UA_CUDA(ua::launch_unpack(usrc, udst, 1, B, s.Nl, H, D, P, stream));
+  {  // 4. all-to-all #2: token block i of every local head goes back to rank i
+    Phase ph(ctx, UA_PHASE_A2A_FWD_OUT, stream);
+    UA_TRY(a2a(ctx, &o_head, &recv_o, 1, size_t(s.chunk()), ncclBfloat16, 2, stream));
+    ctx->a2a_calls += 1;
+  }
+  {  // 5. unpack head chunks -> [B][Nl][H][D]
+    Phase ph(ctx, UA_PHASE_UNPACK_FWD, stream);
+    const void* usrc[1] = {recv_o};
+    void* udst[1] = {out};
+    UA_CUDA(ua::launch_unpack(usrc, udst, 1, B, s.Nl, H, D, P, stream));
+  }
   return UA_OK;
 }
 
@@ -390,18 +449,28 @@ ua_status ua_ulysses_attn_bwd(ua_ctx* ctx, const void* q, const void* k, const v
   UA_TRY(check_device());
   UA_TRY(check_async(ctx));
   char* ws = static_cast<char*>(workspace);
+  const int64_t n_pad = (N + 127) / 128 * 128;
+  const float scale = float(1.0 / std::sqrt(double(D)));
 
   if (P == 1) {
     float* delta = reinterpret_cast<float*>(ws + plan.delta);
     float* dq_acc = reinterpret_cast<float*>(ws + plan.dq_acc);
-    // Delta[n][b][h] = sum_d dO.O (fp32)
-    UA_CUDA(ua::launch_pack(nullptr, nullptr, 0, B, N, H, D, 1, dout, out, delta, stream));
-    UA_CUDA(cudaMemsetAsync(dq_acc, 0, size_t(B * H * ((N + 127) / 128 * 128) * D) * 4, stream));
+    {  // Delta[n][b][h] = sum_d dO.O (fp32)
+      Phase ph(ctx, UA_PHASE_PACK_BWD, stream);
+      UA_CUDA(ua::launch_pack(nullptr, nullptr, 0, B, N, H, D, 1, dout, out, delta, stream));
+    }
     const int64_t sn = int64_t(H) * D, sh = D, sb = N * H * D;
     ua::ViewArg vdk{dk, sn, sh, sb}, vdv{dv, sn, sh, sb}, vdq{dq, sn, sh, sb};
-    UA_TRY(launch_attention_bwd(q, k, v, dout, sn, sh, sb, vdk, vdv, dq_acc, lse, N, int64_t(H) * N, delta,
-                                B * int64_t(H), 1, H, B, N, H, D, stream));
-    UA_CUDA(ua::launch_dq_finalize(dq_acc, vdq, B, N, H, D, float(1.0 / std::sqrt(double(D))), stream));
+    {
+      Phase ph(ctx, UA_PHASE_ATTN_BWD, stream);
+      UA_CUDA(cudaMemsetAsync(dq_acc, 0, size_t(B * H * n_pad * D) * 4, stream));
+      UA_TRY(launch_attention_bwd(q, k, v, dout, sn, sh, sb, vdk, vdv, dq_acc, lse, N, int64_t(H) * N, delta,
+                                  B * int64_t(H), 1, H, B, N, H, D, stream));
+    }
+    {
+      Phase ph(ctx, UA_PHASE_DQ_FINALIZE, stream);
+      UA_CUDA(ua::launch_dq_finalize(dq_acc, vdq, B, N, H, D, scale, stream));
+    }
     return UA_OK;
   }
 
@@ -413,35 +482,68 @@ ua_status ua_ulysses_attn_bwd(ua_ctx* ctx, const void* q, const void* k, const v
   float* dq_acc = reinterpret_cast<float*>(ws + plan.dq_acc);
   void* grad[3] = {ws + plan.grad, ws + plan.grad + S, ws + plan.grad + 2 * S};
   const void* src[4] = {q, k, v, dout};
-  // 1. pack q, k, v, dO + Delta = rowsum(dO * O) in sequence space
-  UA_CUDA(ua::launch_pack(src, send, 4, B, s.Nl, H, D, P, dout, out, send_delta, stream));
-  // 2. all-to-all #3 (fused q, k, v, dO, Delta)
-  UA_NCCL(ncclGroupStart());
-  {
+  {  // 1. pack q, k, v, dO + Delta = rowsum(dO * O) in sequence space
+    Phase ph(ctx, UA_PHASE_PACK_BWD, stream);
+    UA_CUDA(ua::launch_pack(src, send, 4, B, s.Nl, H, D, P, dout, out, send_delta, stream));
+  }
+  {  // 2. all-to-all #3 (fused q, k, v, dO, Delta)
+    Phase ph(ctx, UA_PHASE_A2A_BWD_IN, stream);
+    UA_NCCL(ncclGroupStart());
     ua_status st = a2a(ctx, send, recv, 4, size_t(s.chunk()), ncclBfloat16, 2, stream);
     if (st != UA_OK) { ncclGroupEnd(); return st; }
     void* sd = send_delta;
     void* rd = recv_delta;
     st = a2a(ctx, &sd, &rd, 1, size_t(s.Nl * B * s.Hl), ncclFloat32, 4, stream);
     if (st != UA_OK) { ncclGroupEnd(); return st; }
+    UA_NCCL(ncclGroupEnd());
+    ctx->a2a_calls += 1;
   }
-  UA_NCCL(ncclGroupEnd());
-  ctx->a2a_calls += 1;
   // 3. attention backward on the head shard [N][B][Hl][D]
-  UA_CUDA(cudaMemsetAsync(dq_acc, 0, size_t(B * s.Hl * ((N + 127) / 128 * 128) * D) * 4, stream));
   const int64_t sn = B * int64_t(s.Hl) * D, sh = D, sb = int64_t(s.Hl) * D;
   ua::ViewArg vdq{grad[0], sn, sh, sb}, vdk{grad[1], sn, sh, sb}, vdv{grad[2], sn, sh, sb};
-  UA_TRY(launch_attention_bwd(recv[0], recv[1], recv[2], recv[3], sn, sh, sb, vdk, vdv, dq_acc, lse, N,
-                              int64_t(s.Hl) * N, recv_delta, B * int64_t(s.Hl), 1, s.Hl, B, N, s.Hl, D, stream));
-  UA_CUDA(ua::launch_dq_finalize(dq_acc, vdq, B, N, s.Hl, D, float(1.0 / std::sqrt(double(D))), stream));
-  // 4. all-to-all #4 (fused dq, dk, dv) back to the token owners
+  {
+    Phase ph(ctx, UA_PHASE_ATTN_BWD, stream);
+    UA_CUDA(cudaMemsetAsync(dq_acc, 0, size_t(B * s.Hl * n_pad * D) * 4, stream));
+    UA_TRY(launch_attention_bwd(recv[0], recv[1], recv[2], recv[3], sn, sh, sb, vdk, vdv, dq_acc, lse, N,
+                                int64_t(s.Hl) * N, recv_delta, B * int64_t(s.Hl), 1, s.Hl, B, N, s.Hl, D, stream));
+  }
+  {
+    Phase ph(ctx, UA_PHASE_DQ_FINALIZE, stream);
+    UA_CUDA(ua::launch_dq_finalize(dq_acc, vdq, B, N, s.Hl, D, scale, stream));
+  }
   void* rgrad[3] = {ws + plan.send, ws + plan.send + S, ws + plan.send + 2 * S};
-  UA_TRY(a2a(ctx, grad, rgrad, 3, size_t(s.chunk()), ncclBfloat16, 2, stream));
-  ctx->a2a_calls += 1;
-  // 5. unpack -> dq, dk, dv [B][Nl][H][D]
-  const void* usrc[3] = {rgrad[0], rgrad[1], rgrad[2]};
-  void* udst[3] = {dq, dk, dv};
-  UA_CUDA(ua::launch_unpack(usrc, udst, 3, B, s.Nl, H, D, P, stream));
+  {  // 4. all-to-all #4 (fused dq, dk, dv) back to the token owners
+    Phase ph(ctx, UA_PHASE_A2A_BWD_OUT, stream);
+    UA_TRY(a2a(ctx, grad, rgrad, 3, size_t(s.chunk()), ncclBfloat16, 2, stream));
+    ctx->a2a_calls += 1;
+  }
+  {  // 5. unpack -> dq, dk, dv [B][Nl][H][D]
+    Phase ph(ctx, UA_PHASE_UNPACK_BWD, stream);
+    const void* usrc[3] = {rgrad[0], rgrad[1], rgrad[2]};
+    void* udst[3] = {dq, dk, dv};
+    UA_CUDA(ua::launch_unpack(usrc, udst, 3, B, s.Nl, H, D, P, stream));
+  }
+  return UA_OK;
+}
+
+ua_status ua_ctx_enable_timing(ua_ctx* ctx, int enable) {
+  if (!ctx) return fail(UA_ERR_INVALID_ARG, "ctx is NULL");
+  ctx->timing = enable != 0;
+  return UA_OK;
+}
+
+ua_status ua_ctx_phase_times(ua_ctx* ctx, double* ms, int64_t* launches) {
+  if (!ctx) return fail(UA_ERR_INVALID_ARG, "ctx is NULL");
+  for (auto& r : ctx->pending) {
+    UA_CUDA(cudaEventSynchronize(r.b));
+    float t = 0.f;
+    UA_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
+    if (ms) ms[r.phase] += double(t);
+    if (launches) launches[r.phase] += 1;
+    ctx->pool.push_back(r.a);
+    ctx->pool.push_back(r.b);
+  }
+  ctx->pending.clear();
   return UA_OK;
 }
 
