@@ -1,0 +1,107 @@
+"""P > 1: real NCCL ranks on the GPU box (gpu), and the host-side multi-rank
+logic over gloo on CPU (world_size 2; no GPU needed)."""
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def torchrun(nproc, script, *args, timeout=900, env=None):
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+           "--master-addr=127.0.0.1", f"--master-port={29500 + os.getpid() % 1000}", script, *args]
+    e = dict(os.environ, **(env or {}))
+    e["PYTHONPATH"] = ROOT + os.pathsep + e.get("PYTHONPATH", "")
+    return subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=timeout, env=e)
+
+
+# ----------------------------------------------------------------- GPU, NCCL
+@pytest.mark.gpu
+@pytest.mark.parametrize("P,N,H,D,sigma", [
+    (2, 4096, 8, 64, 1.0),
+    (2, 2048, 4, 128, 2.0),
+    (2, 4050, 4, 64, 1.0),      # ragged per-rank tail: N/P = 2025
+    (4, 4096, 8, 64, 1.0),
+    (8, 8192, 16, 64, 1.0),
+    (8, 2048, 8, 32, 2.0),
+])
+def test_ulysses_p_way(P, N, H, D, sigma):
+    if torch.cuda.device_count() < P:
+        pytest.skip(f"needs {P} GPUs")
+    r = torchrun(P, os.path.join(ROOT, "tests", "mp_ulysses_check.py"), f"--N={N}", f"--H={H}", f"--D={D}",
+                 f"--sigma={sigma}")
+    assert r.returncode == 0 and "MP_OK" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
+
+
+# ----------------------------------------------------------------- CPU, gloo
+GLOO_SCRIPT = r'''
+import os, sys, numpy as np, torch, torch.distributed as dist
+sys.path.insert(0, os.environ["UA_ROOT"])
+import oracle, paper_2405_15780_b200 as ua
+from oracle import ulysses
+dist.init_process_group("gloo")
+rank, P = dist.get_rank(), dist.get_world_size()
+# 1) validation is host-only and identical on every rank (S:248 head limit)
+codes = [ua.lib().ua_validate(1, 16, 1, 64, P), ua.lib().ua_validate(1, 15, 4, 64, P),
+         ua.lib().ua_validate(1, 16, 4, 64, P)]
+allc = [None] * P
+dist.all_gather_object(allc, codes)
+assert all(c == [2, 3, 0] for c in allc), allc
+# 2) the oracle's all-to-all (S:122) equals torch.distributed.all_to_all (library routine)
+B, N, H, D = 1, 8, 4, 2
+x = np.arange(B * N * H * D, dtype=np.float64).reshape(B, N, H, D)
+shards = ulysses.shard_seq(x, P)
+mine = torch.from_numpy(shards[rank].copy())
+hl = H // P
+send = [mine[:, :, j * hl:(j + 1) * hl].contiguous() for j in range(P)]
+recv = [torch.empty_like(send[0]) for _ in range(P)]
+reqs = []  # gloo has no all_to_all: exchange point-to-point (output[j] on rank i = input[i] on rank j)
+for j in range(P):
+    if j == rank:
+        recv[j].copy_(send[j])
+    else:
+        reqs += [dist.isend(send[j], j), dist.irecv(recv[j], j)]
+for r in reqs:
+    r.wait()
+got = torch.cat(recv, dim=1).numpy()
+exp = ulysses.seq_to_head(shards, P)[rank]
+assert np.array_equal(got, exp)
+# 3) the library's unique id (128 bytes) travels over a torch process group
+uid = [ua.get_unique_id() if rank == 0 else None]
+dist.broadcast_object_list(uid, src=0)
+assert isinstance(uid[0], bytes) and len(uid[0]) == 128
+# 4) workspace plans agree across ranks
+ws = [None] * P
+dist.all_gather_object(ws, ua.workspace_size(1, 188416, 32, 64, P))
+assert len(set(ws)) == 1
+if rank == 0:
+    print("GLOO_OK", flush=True)
+dist.destroy_process_group()
+'''
+
+
+def test_gloo_two_ranks(tmp_path):
+    from paper_2405_15780_b200 import build
+    build.build()
+    script = tmp_path / "gloo_check.py"
+    script.write_text(GLOO_SCRIPT)
+    r = torchrun(2, str(script), timeout=300, env={"UA_ROOT": ROOT})
+    assert r.returncode == 0 and "GLOO_OK" in r.stdout, r.stdout[-2000:] + r.stderr[-3000:]
+
+
+def test_bench_reference_arm_two_ranks():
+    """bench.py --impl reference under torchrun: rank 0 prints one JSON line,
+    the other rank exits 0 without work."""
+    r = torchrun(2, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "1", "--warmup", "1",
+                 "--gpus", "2", timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    import json
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["unit"] == "TFLOP/s" and d["value"] > 0
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["cpu_baseline"]["kind"] == "oracle"
