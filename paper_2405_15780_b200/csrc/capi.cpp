@@ -256,6 +256,9 @@ ua_status launch_attention_bwd(const void* q, const void* k, const void* v, cons
   UA_TRY(make_map(&p.tm_k, k, D, N, heads, B, sn, sh, sb));
   UA_TRY(make_map(&p.tm_v, v, D, N, heads, B, sn, sh, sb));
   UA_TRY(make_map(&p.tm_do, dout, D, N, heads, B, sn, sh, sb));
+  const int64_t n_pad = (N + 127) / 128 * 128;
+  if (!ua::make_tmap_f32_2d(&p.tm_dq, dq_acc, uint64_t(D), uint64_t(B * heads * n_pad), 128))
+    return fail(UA_ERR_CUDA, "cuTensorMapEncodeTiled failed for dq_acc");
   p.dk = dk;
   p.dv = dv;
   p.dq_acc = dq_acc;

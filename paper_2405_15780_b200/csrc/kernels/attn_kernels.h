@@ -32,6 +32,7 @@ struct alignas(64) BwdParams {
   CUtensorMap tm_k;
   CUtensorMap tm_v;
   CUtensorMap tm_do;
+  CUtensorMap tm_dq;  // fp32 2-D {D, B*heads*N_pad} over dq_acc, box {32, 128}, SW128 (reduce-add target)
   ViewArg dk, dv;     // bf16 outputs
   float* dq_acc;      // fp32 [B*heads][N_pad][D] accumulator, N_pad = ceil(N/128)*128 (zeroed by caller)
   const float* lse;   // lse[b*l_sb + h*l_sh + n]
@@ -46,6 +47,7 @@ struct alignas(64) BwdParams {
 
 cudaError_t launch_attn_fwd(const FwdParams& p, int D, int B, int heads, cudaStream_t stream);
 cudaError_t launch_attn_bwd(const BwdParams& p, int D, int B, int heads, cudaStream_t stream);
+cudaError_t launch_attn_bwd_v2(const BwdParams& p, int D, int B, int heads, cudaStream_t stream);
 
 // ---- layout / elementwise kernels (layout.cu) --------------------------------
 // Sequence shard -> per-destination send chunks, for `ntensors` tensors:
