@@ -268,6 +268,7 @@ ua_status launch_attention_bwd(const void* q, const void* k, const void* v, cons
   p.d_sn = d_sn; p.d_sh = d_sh; p.d_sb = d_sb;
   p.n = int(N);
   p.heads = heads;
+  p.batch = int(B);
   p.scale = float(1.0 / std::sqrt(double(D)));
   p.scale_log2 = float(1.4426950408889634 / std::sqrt(double(D)));
   UA_CUDA(ua::launch_attn_bwd(p, D, int(B), heads, stream));

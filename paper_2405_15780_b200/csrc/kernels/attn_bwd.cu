@@ -319,13 +319,13 @@ cudaError_t launch_bwd_impl(const BwdParams& p, int B, int heads, cudaStream_t s
 }  // namespace
 
 cudaError_t launch_attn_bwd(const BwdParams& p, int D, int B, int heads, cudaStream_t stream) {
-  // D <= 64: the overlapped v2 kernel (attn_bwd_v2.cu); UA_BWD_KERNEL=v1 forces
+  // D <= 64: the persistent warp-specialised kernel (attn_bwd_ws.cu); UA_BWD_KERNEL=v1 forces
   // this file's kernel (kept for D = 128 and for A/B measurements).
   static const bool force_v1 = [] {
     const char* e = std::getenv("UA_BWD_KERNEL");
     return e != nullptr && std::strcmp(e, "v1") == 0;
   }();
-  if (D <= 64 && !force_v1) return launch_attn_bwd_v2(p, D, B, heads, stream);
+  if (D <= 64 && !force_v1) return launch_attn_bwd_ws(p, D, stream);
   switch (D) {
     case 32: return launch_bwd_impl<32>(p, B, heads, stream);
     case 64: return launch_bwd_impl<64>(p, B, heads, stream);

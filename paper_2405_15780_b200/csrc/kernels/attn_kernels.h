@@ -41,13 +41,14 @@ struct alignas(64) BwdParams {
   int64_t d_sn, d_sh, d_sb;
   int n;              // sequence length (queries == keys)
   int heads;
+  int batch;
   float scale;        // 1/sqrt(D)
   float scale_log2;   // log2(e)/sqrt(D)
 };
 
 cudaError_t launch_attn_fwd(const FwdParams& p, int D, int B, int heads, cudaStream_t stream);
 cudaError_t launch_attn_bwd(const BwdParams& p, int D, int B, int heads, cudaStream_t stream);
-cudaError_t launch_attn_bwd_v2(const BwdParams& p, int D, int B, int heads, cudaStream_t stream);
+cudaError_t launch_attn_bwd_ws(const BwdParams& p, int D, cudaStream_t stream);
 
 // ---- layout / elementwise kernels (layout.cu) --------------------------------
 // Sequence shard -> per-destination send chunks, for `ntensors` tensors:
