@@ -166,7 +166,7 @@ FwdPlan plan_fwd(const Shape& s) {
   return p;
 }
 struct BwdPlan {
-  size_t send = 0, send_delta = 0, recv = 0, recv_delta = 0, dq_acc = 0, grad = 0, delta = 0, total = 0;
+  size_t send = 0, send_delta = 0, recv = 0, recv_delta = 0, dq_acc = 0, grad = 0, delta = 0, lsed = 0, total = 0;
 };
 BwdPlan plan_bwd(const Shape& s) {
   BwdPlan p;
@@ -177,7 +177,8 @@ BwdPlan plan_bwd(const Shape& s) {
   if (s.P == 1) {
     p.delta = 0;                                  // [N][B][H] fp32
     p.dq_acc = align_up(DL);                      // [B*H][N_pad][D] fp32
-    p.total = align_up(p.dq_acc + DQ);
+    p.lsed = align_up(p.dq_acc + DQ);             // [B*H][N_pad] float2 (-lse*log2e, Delta)
+    p.total = align_up(p.lsed + size_t(s.B * s.Hl * n_pad) * 8);
     return p;
   }
   p.send = 0;                                     // [4][P][Nl][B][Hl][D]; reused as recv_grad [3][P]...
@@ -186,7 +187,8 @@ BwdPlan plan_bwd(const Shape& s) {
   p.recv_delta = align_up(p.recv + 4 * S);        // [N][B][Hl]
   p.dq_acc = align_up(p.recv_delta + DL);         // [B*Hl][N_pad][D] fp32
   p.grad = align_up(p.dq_acc + DQ);               // [3][N][B][Hl][D] bf16
-  p.total = align_up(p.grad + 3 * S);
+  p.lsed = align_up(p.grad + 3 * S);              // [B*Hl][N_pad] float2
+  p.total = align_up(p.lsed + size_t(s.B * s.Hl * n_pad) * 8);
   return p;
 }
 
@@ -249,9 +251,13 @@ ua_status launch_attention_fwd(const void* q, const void* k, const void* v, int6
 ua_status launch_attention_bwd(const void* q, const void* k, const void* v, const void* dout, int64_t sn, int64_t sh,
                                int64_t sb, ua::ViewArg dk, ua::ViewArg dv, float* dq_acc, const float* lse,
                                int64_t l_sh, int64_t l_sb, const float* delta, int64_t d_sn, int64_t d_sh,
-                               int64_t d_sb, int64_t B, int64_t N, int heads, int D, cudaStream_t stream) {
+                               int64_t d_sb, int64_t B, int64_t N, int heads, int D, float2* lsed,
+                               cudaStream_t stream) {
   ua::BwdParams p;
   std::memset(&p, 0, sizeof(p));
+  // (-lse*log2e, Delta) per query row, contiguous per head (bulk-loaded by the kernel)
+  UA_CUDA(ua::launch_bwd_prep(lse, l_sh, l_sb, delta, d_sn, d_sh, d_sb, lsed, B, heads, N, stream));
+  p.lsed = lsed;
   UA_TRY(make_map(&p.tm_q, q, D, N, heads, B, sn, sh, sb));
   UA_TRY(make_map(&p.tm_k, k, D, N, heads, B, sn, sh, sb));
   UA_TRY(make_map(&p.tm_v, v, D, N, heads, B, sn, sh, sb));
@@ -469,7 +475,8 @@ ua_status ua_ulysses_attn_bwd(ua_ctx* ctx, const void* q, const void* k, const v
       Phase ph(ctx, UA_PHASE_ATTN_BWD, stream);
       UA_CUDA(cudaMemsetAsync(dq_acc, 0, size_t(B * H * n_pad * D) * 4, stream));
       UA_TRY(launch_attention_bwd(q, k, v, dout, sn, sh, sb, vdk, vdv, dq_acc, lse, N, int64_t(H) * N, delta,
-                                  B * int64_t(H), 1, H, B, N, H, D, stream));
+                                  B * int64_t(H), 1, H, B, N, H, D, reinterpret_cast<float2*>(ws + plan.lsed),
+                                  stream));
     }
     {
       Phase ph(ctx, UA_PHASE_DQ_FINALIZE, stream);
@@ -509,7 +516,8 @@ ua_status ua_ulysses_attn_bwd(ua_ctx* ctx, const void* q, const void* k, const v
     Phase ph(ctx, UA_PHASE_ATTN_BWD, stream);
     UA_CUDA(cudaMemsetAsync(dq_acc, 0, size_t(B * s.Hl * n_pad * D) * 4, stream));
     UA_TRY(launch_attention_bwd(recv[0], recv[1], recv[2], recv[3], sn, sh, sb, vdk, vdv, dq_acc, lse, N,
-                                int64_t(s.Hl) * N, recv_delta, B * int64_t(s.Hl), 1, s.Hl, B, N, s.Hl, D, stream));
+                                int64_t(s.Hl) * N, recv_delta, B * int64_t(s.Hl), 1, s.Hl, B, N, s.Hl, D,
+                                reinterpret_cast<float2*>(ws + plan.lsed), stream));
   }
   {
     Phase ph(ctx, UA_PHASE_DQ_FINALIZE, stream);

@@ -36,8 +36,11 @@ struct BwdWsCfg {
   static constexpr int kStagger = 16;
   static constexpr uint32_t kColS = 0, kColDP = 128, kColDV = 256, kColDK = 256 + D, kColDQ = 256 + 2 * D;
   static constexpr int kDsBytes = 128 * 128 * 2;
-  static constexpr int kStageBytes = 128 * D * 4;
-  static constexpr int kSmemBytes = 1024 + 6 * G::kTileBytes + 2 * kDsBytes + kStageBytes + 2 * 128 * 8 + 256;
+  static constexpr int kStages = 3;                 // Q / dO / (lse, Delta) ring depth
+  static constexpr int kStageBytes = 128 * 32 * 4;  // one 32-column fp32 box of the dQ tile
+  static constexpr int kLsedBytes = 128 * 8;        // (-lse*log2e, Delta) per query row
+  static constexpr int kSmemBytes = 1024 + (2 + 2 * kStages) * G::kTileBytes + 2 * kDsBytes + kStageBytes +
+                                    kStages * kLsedBytes + 256;
   static_assert(256 + 3 * D <= 512, "TMEM budget");
 };
 
@@ -49,25 +52,25 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_ws_kernel(const __grid_consta
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sK = smem;
   uint8_t* sV = sK + G::kTileBytes;
-  uint8_t* sQ = sV + G::kTileBytes;               // [2]
-  uint8_t* sdO = sQ + 2 * G::kTileBytes;          // [2]
-  uint8_t* sdS = sdO + 2 * G::kTileBytes;         // [2] dS^T [128 keys][128 q] bf16 (2 SW128 atoms)
-  uint8_t* sStage = sdS + 2 * C::kDsBytes;        // dQ tile: D/32 SW128 boxes [128][32] fp32
-  float* s_nlse = reinterpret_cast<float*>(sStage + C::kStageBytes);  // [2][128]
-  float* s_dlt = s_nlse + 2 * 128;                                    // [2][128]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(s_dlt + 2 * 128);
+  constexpr int kS = C::kStages;
+  uint8_t* sQ = sV + G::kTileBytes;               // [kS]
+  uint8_t* sdO = sQ + kS * G::kTileBytes;         // [kS]
+  uint8_t* sdS = sdO + kS * G::kTileBytes;        // [2] dS^T [128 keys][128 q] bf16 (2 SW128 atoms)
+  uint8_t* sStage = sdS + 2 * C::kDsBytes;        // one SW128 box [128][32] fp32 of the dQ tile
+  float2* s_lsed = reinterpret_cast<float2*>(sStage + C::kStageBytes);  // [kS][128] (-lse*log2e, Delta)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(s_lsed + kS * 128);
   uint64_t* kv_full = bars + 0;
   uint64_t* kv_empty = bars + 1;
-  uint64_t* qdo_full = bars + 2;      // [2]
-  uint64_t* qdo_empty = bars + 4;     // [2]
-  uint64_t* sdp_full = bars + 6;      // [2] per half
-  uint64_t* ds_ready = bars + 8;      // [2] per half
-  uint64_t* ds_free = bars + 10;      // [2] per dS buffer
-  uint64_t* dq_full = bars + 12;
-  uint64_t* dq_empty = bars + 13;
-  uint64_t* acc_full = bars + 14;
-  uint64_t* acc_free = bars + 15;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
+  uint64_t* sdp_full = bars + 2;      // [2] per half
+  uint64_t* ds_ready = bars + 4;      // [2] per half
+  uint64_t* ds_free = bars + 6;       // [2] per dS buffer
+  uint64_t* dq_full = bars + 8;
+  uint64_t* dq_empty = bars + 9;
+  uint64_t* acc_full = bars + 10;
+  uint64_t* acc_free = bars + 11;
+  uint64_t* qdo_full = bars + 12;     // [kS]
+  uint64_t* qdo_empty = qdo_full + kS;  // [kS]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(qdo_empty + kS);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -79,9 +82,11 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_ws_kernel(const __grid_consta
   if (threadIdx.x == 0) {
     mbar_init(kv_full, 1);
     mbar_init(kv_empty, 1);
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(&qdo_full[s], 32);
+    for (int s = 0; s < kS; ++s) {
+      mbar_init(&qdo_full[s], 1);
       mbar_init(&qdo_empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
       mbar_init(&sdp_full[s], 1);
       mbar_init(&ds_ready[s], 128);
       mbar_init(&ds_free[s], 1);
@@ -106,43 +111,31 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_ws_kernel(const __grid_consta
       tma_prefetch_desc(&p.tm_v);
       tma_prefetch_desc(&p.tm_do);
     }
-    int T = 0, it = 0;
-    for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
-      const int kt = item % n_kt, bh = item / n_kt;
-      const int b = bh / p.heads, h = bh % p.heads;
-      if (lane == 0) {
+    if (lane == 0) {
+      int T = 0, it = 0;
+      const int n_pad = n_q * 128;
+      for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
+        const int kt = item % n_kt, bh = item / n_kt;
+        const int b = bh / p.heads, h = bh % p.heads;
         if (it > 0) mbar_wait(kv_empty, (it - 1) & 1);
         mbar_arrive_expect_tx(kv_full, 2 * G::kTileBytes);
         for (int a = 0; a < G::kAtoms; ++a) {
           tma_load_4d(sK + a * G::kAtomBytes, &p.tm_k, kv_full, a * G::kAtomCols, kt * 128, h, b, kEvictFirst);
           tma_load_4d(sV + a * G::kAtomBytes, &p.tm_v, kv_full, a * G::kAtomCols, kt * 128, h, b, kEvictFirst);
         }
-      }
-      const float* lse_bh = p.lse + b * p.l_sb + h * p.l_sh;
-      const float* dlt_bh = p.delta + b * p.d_sb + h * p.d_sh;
-      for (int t = 0; t < n_q; ++t, ++T) {
-        const int s = T & 1;
-        const int tile = (start + t) % n_q;
-        if (T >= 2) mbar_wait(&qdo_empty[s], ((T >> 1) & 1) ^ 1);
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          const int row = r * 32 + lane;
-          const int qi = tile * 128 + row;
-          const bool ok = qi < p.n;
-          s_nlse[s * 128 + row] = ok ? -lse_bh[qi] * kLog2e : -INFINITY;
-          s_dlt[s * 128 + row] = ok ? dlt_bh[int64_t(qi) * p.d_sn] : 0.f;
-        }
-        __syncwarp();
-        if (lane == 0) {
-          mbar_arrive_expect_tx(&qdo_full[s], 2 * G::kTileBytes);
+        const float2* lsed_bh = p.lsed + int64_t(bh) * n_pad;
+        for (int t = 0; t < n_q; ++t, ++T) {
+          const int s = T % kS;
+          const int tile = (start + t) % n_q;
+          if (T >= kS) mbar_wait(&qdo_empty[s], ((T / kS) & 1) ^ 1);
+          mbar_arrive_expect_tx(&qdo_full[s], 2 * G::kTileBytes + C::kLsedBytes);
           for (int a = 0; a < G::kAtoms; ++a) {
             tma_load_4d(sQ + s * G::kTileBytes + a * G::kAtomBytes, &p.tm_q, &qdo_full[s], a * G::kAtomCols,
                         tile * 128, h, b, kEvictLast);
             tma_load_4d(sdO + s * G::kTileBytes + a * G::kAtomBytes, &p.tm_do, &qdo_full[s], a * G::kAtomCols,
                         tile * 128, h, b, kEvictLast);
           }
-        } else {
-          mbar_arrive(&qdo_full[s]);
+          bulk_load(s_lsed + s * 128, lsed_bh + tile * 128, C::kLsedBytes, &qdo_full[s]);
         }
       }
     }
@@ -155,7 +148,7 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_ws_kernel(const __grid_consta
       const uint32_t sKa = smem_u32(sK), sVa = smem_u32(sV), sQa = smem_u32(sQ), sdOa = smem_u32(sdO);
       const uint32_t sdSa = smem_u32(sdS);
       auto issue_sdp = [&](int T, int hh) {
-        const int s = T & 1;
+        const int s = T % kS;
         const uint32_t qt = sQa + s * G::kTileBytes + 64 * hh * G::kSw;
         const uint32_t dot = sdOa + s * G::kTileBytes + 64 * hh * G::kSw;
 #pragma unroll
@@ -171,7 +164,7 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_ws_kernel(const __grid_consta
       int T = 0, it = 0;
       for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
         mbar_wait(kv_full, it & 1);
-        mbar_wait(&qdo_full[T & 1], (T >> 1) & 1);
+        mbar_wait(&qdo_full[T % kS], (T / kS) & 1);
         tc_fence_after();
         issue_sdp(T, 0);
         issue_sdp(T, 1);
@@ -180,7 +173,7 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_ws_kernel(const __grid_consta
           tc_fence_after();
         }
         for (int t = 0; t < n_q; ++t, ++T) {
-          const int s = T & 1;
+          const int s = T % kS;
           const uint32_t qt = sQa + s * G::kTileBytes, dot = sdOa + s * G::kTileBytes;
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {
@@ -211,7 +204,7 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_ws_kernel(const __grid_consta
             }
             if (t + 1 < n_q) {
               if (hh == 0) {
-                mbar_wait(&qdo_full[(T + 1) & 1], ((T + 1) >> 1) & 1);
+                mbar_wait(&qdo_full[(T + 1) % kS], ((T + 1) / kS) & 1);
                 tc_fence_after();
               }
               issue_sdp(T + 1, hh);
@@ -236,14 +229,13 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_ws_kernel(const __grid_consta
       const int kt = item % n_kt, bh = item / n_kt;
       const int b = bh / p.heads, h = bh % p.heads;
       for (int t = 0; t < n_q; ++t, ++T) {
-        const int s = T & 1;
-        mbar_wait(&qdo_full[s], (T >> 1) & 1);                       // lse / Delta visibility
+        const int s = T % kS;
+        mbar_wait(&qdo_full[s], (T / kS) & 1);                       // (lse, Delta) landed
         if (T >= 2) mbar_wait(&ds_free[T & 1], ((T >> 1) & 1) ^ 1);  // dS buffer consumed by dQ(T-2)
         mbar_wait(&sdp_full[hh], T & 1);
         tc_fence_after();
         uint8_t* atom = sdS + (T & 1) * C::kDsBytes + hh * (128 * 128) + j * 128;
-        const float4* nl4 = reinterpret_cast<const float4*>(s_nlse + s * 128 + 64 * hh);
-        const float4* dl4 = reinterpret_cast<const float4*>(s_dlt + s * 128 + 64 * hh);
+        const float4* ld4 = reinterpret_cast<const float4*>(s_lsed + s * 128 + 64 * hh);  // (nl0, d0, nl1, d1)
 #pragma unroll
         for (int cc = 0; cc < 64; cc += 16) {
           uint32_t rs[16], rd[16];
@@ -252,19 +244,13 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_ws_kernel(const __grid_consta
           tmem_ld_wait();
           uint32_t pk_p[8], pk_ds[8];
 #pragma unroll
-          for (int x = 0; x < 16; x += 4) {
-            const float4 nl = nl4[(cc + x) / 4];
-            const float4 dl = dl4[(cc + x) / 4];
-            const float p0 = ex2(fmaf(__uint_as_float(rs[x + 0]), c, nl.x));
-            const float p1 = ex2(fmaf(__uint_as_float(rs[x + 1]), c, nl.y));
-            const float p2 = ex2(fmaf(__uint_as_float(rs[x + 2]), c, nl.z));
-            const float p3 = ex2(fmaf(__uint_as_float(rs[x + 3]), c, nl.w));
+          for (int x = 0; x < 16; x += 2) {
+            const float4 ld = ld4[(cc + x) / 2];
+            const float p0 = ex2(fmaf(__uint_as_float(rs[x + 0]), c, ld.x));
+            const float p1 = ex2(fmaf(__uint_as_float(rs[x + 1]), c, ld.z));
             pk_p[x / 2] = pack_bf16x2(p0, p1);
-            pk_p[x / 2 + 1] = pack_bf16x2(p2, p3);
-            pk_ds[x / 2] = pack_bf16x2(p0 * (__uint_as_float(rd[x + 0]) - dl.x),
-                                       p1 * (__uint_as_float(rd[x + 1]) - dl.y));
-            pk_ds[x / 2 + 1] = pack_bf16x2(p2 * (__uint_as_float(rd[x + 2]) - dl.z),
-                                           p3 * (__uint_as_float(rd[x + 3]) - dl.w));
+            pk_ds[x / 2] = pack_bf16x2(p0 * (__uint_as_float(rd[x + 0]) - ld.y),
+                                       p1 * (__uint_as_float(rd[x + 1]) - ld.w));
           }
           tmem_st8(t_lane + colS + cc / 2, pk_p);
           tmem_st8(t_lane + colDP + cc / 2, pk_ds);
@@ -331,23 +317,22 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_ws_kernel(const __grid_consta
         }
         tc_fence_before();
         mbar_arrive(dq_empty);
-        if (leader) bulk_wait_read<0>();   // previous reduction has read the staging tile
-        named_bar_sync(1, 128);
         uint8_t* srow = sStage + r * 128;
 #pragma unroll
-        for (int cb = 0; cb < D / 32; ++cb)
+        for (int cb = 0; cb < D / 32; ++cb) {
+          if (leader) bulk_wait_read<0>();   // previous reduction has read the staging box
+          named_bar_sync(1, 128);
 #pragma unroll
           for (int q4 = 0; q4 < 8; ++q4)
-            *reinterpret_cast<float4*>(srow + cb * 16384 + ((q4 ^ (r & 7)) * 16)) =
+            *reinterpret_cast<float4*>(srow + ((q4 ^ (r & 7)) * 16)) =
                 make_float4(acc[32 * cb + 4 * q4], acc[32 * cb + 4 * q4 + 1], acc[32 * cb + 4 * q4 + 2],
                             acc[32 * cb + 4 * q4 + 3]);
-        fence_proxy_async_smem();
-        named_bar_sync(1, 128);
-        if (leader) {
-          const int row0 = bh * n_pad + tile * 128;
-#pragma unroll
-          for (int cb = 0; cb < D / 32; ++cb) tma_reduce_add_2d(&p.tm_dq, sStage + cb * 16384, 32 * cb, row0);
-          bulk_commit();
+          fence_proxy_async_smem();
+          named_bar_sync(1, 128);
+          if (leader) {
+            tma_reduce_add_2d(&p.tm_dq, sStage, 32 * cb, bh * n_pad + tile * 128);
+            bulk_commit();
+          }
         }
       }
     }

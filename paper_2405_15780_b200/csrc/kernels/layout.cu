@@ -118,6 +118,19 @@ __global__ void __launch_bounds__(256) lse_merge_kernel(float* __restrict__ o_a,
   }
 }
 
+__global__ void __launch_bounds__(256) bwd_prep_kernel(const float* __restrict__ lse, int64_t l_sh, int64_t l_sb,
+                                                       const float* __restrict__ delta, int64_t d_sn, int64_t d_sh,
+                                                       int64_t d_sb, float2* __restrict__ lsed, int heads, int64_t N,
+                                                       int64_t n_pad, int64_t total) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t n = i % n_pad, bh = i / n_pad;
+    const int64_t b = bh / heads, h = bh % heads;
+    float2 v = make_float2(-INFINITY, 0.f);
+    if (n < N) v = make_float2(-lse[b * l_sb + h * l_sh + n] * 1.4426950408889634f, delta[b * d_sb + h * d_sh + n * d_sn]);
+    lsed[i] = v;
+  }
+}
+
 int grid_for(int64_t work, int threads) {
   int64_t g = (work + threads - 1) / threads;
   const int64_t cap = 148 * 16;  // 16 resident 256-thread blocks per SM
@@ -182,6 +195,16 @@ cudaError_t launch_f32_to_view(const float* src, ViewArg dst, int64_t B, int64_t
   const int64_t total_vec = B * heads * N * (D / 8);
   f32_to_bf16_view_kernel<<<grid_for(total_vec, 256), 256, 0, stream>>>(reinterpret_cast<const float4*>(src), dst, N,
                                                                          N, heads, D, 1.0f, total_vec);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_bwd_prep(const float* lse, int64_t l_sh, int64_t l_sb, const float* delta, int64_t d_sn,
+                            int64_t d_sh, int64_t d_sb, float2* lsed, int64_t B, int heads, int64_t N,
+                            cudaStream_t stream) {
+  const int64_t n_pad = (N + 127) / 128 * 128;
+  const int64_t total = B * heads * n_pad;
+  bwd_prep_kernel<<<grid_for(total, 256), 256, 0, stream>>>(lse, l_sh, l_sb, delta, d_sn, d_sh, d_sb, lsed, heads, N,
+                                                            n_pad, total);
   return cudaGetLastError();
 }
 
