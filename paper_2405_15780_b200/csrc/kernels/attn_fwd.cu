@@ -41,6 +41,7 @@ struct FwdCfg {
   static constexpr uint32_t kColS = 0;     // + t*128
   static constexpr uint32_t kColO = 256;   // + t*D
   static constexpr float kRescaleThreshold = 8.0f;  // log2 units
+  static constexpr bool kPolyExp = D <= 64;          // exp unit co-binds only at small D
 };
 
 template <int D>
@@ -206,8 +207,12 @@ __global__ void __launch_bounds__(384, 1) attn_fwd_kernel(const __grid_constant_
         uint32_t pk[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          const float p0 = ex2(fmaf(sv[cc + 2 * i], c, neg_m));
-          const float p1 = ex2(fmaf(sv[cc + 2 * i + 1], c, neg_m));
+          const float x0 = fmaf(sv[cc + 2 * i], c, neg_m);
+          const float x1 = fmaf(sv[cc + 2 * i + 1], c, neg_m);
+          // 6 of every 16 pairs on the FMA pipe, the rest on MUFU (D <= 64: MUFU-bound)
+          const bool poly = C::kPolyExp && (i & 7) < 3;
+          const float p0 = poly ? exp2_poly(x0) : ex2(x0);
+          const float p1 = poly ? exp2_poly(x1) : ex2(x1);
           ls[i % 4] += p0 + p1;
           pk[i] = pack_bf16x2(p0, p1);
         }

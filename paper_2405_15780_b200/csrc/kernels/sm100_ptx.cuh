@@ -233,6 +233,18 @@ __device__ __forceinline__ float ex2(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+// 2^x on the FMA pipe (offloads the MUFU unit): round-to-nearest split
+// x = j + f, f in [-1/2, 1/2], via the 1.5*2^23 shifter; 2^f by a degree-3
+// polynomial (max relative error 2.2e-4, far below bf16's 2^-8 rounding of P);
+// 2^j added into the exponent bits.  x is clamped at -126 (result ~1e-38).
+__device__ __forceinline__ float exp2_poly(float x) {
+  x = fmaxf(x, -126.f);
+  const float t = x + 12582912.f;
+  const float j = t - 12582912.f;
+  const float f = x - j;
+  const float p = fmaf(fmaf(fmaf(0.05286738f, f, 0.24215202f), f, 0.69358677f), f, 0.99996275f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);  // .x = lo (low 16 bits)
   return *reinterpret_cast<uint32_t*>(&v);
