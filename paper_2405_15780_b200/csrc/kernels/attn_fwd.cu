@@ -186,12 +186,14 @@ __global__ void __launch_bounds__(384, 1) attn_fwd_kernel(const __grid_constant_
         for (int i = 0; i < 128; ++i)
           if (kv0 + i >= p.kv_end) sv[i] = -INFINITY;
       }
-      float mx[8];
+      // row max: 3-input FMNMX, 4 independent chains
+      float mx[4] = {sv[0], sv[1], sv[2], sv[3]};
 #pragma unroll
-      for (int i = 0; i < 8; ++i) mx[i] = sv[i];
+      for (int i = 4; i < 128; i += 8) {
 #pragma unroll
-      for (int i = 8; i < 128; ++i) mx[i % 8] = fmaxf(mx[i % 8], sv[i]);
-      float rmax = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])), fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
+        for (int u = 0; u < 4; ++u) mx[u] = fmax3(mx[u], sv[i + 2 * u], sv[i + 2 * u + 1]);
+      }
+      const float rmax = fmax3(mx[0], mx[1], fmaxf(mx[2], mx[3]));
       const float m_new = fmaxf(m_use, rmax * c);
       const bool need = m_new > m_use + C::kRescaleThreshold;
       const bool warp_need = __any_sync(0xffffffffu, need);
@@ -200,25 +202,25 @@ __global__ void __launch_bounds__(384, 1) attn_fwd_kernel(const __grid_constant_
         m_use = m_new;
         l *= alpha;
       }
-      const float neg_m = -m_use;
-      float ls[4] = {0.f, 0.f, 0.f, 0.f};
+      // p = 2^(s*c - m): packed fp32x2 FFMA for the argument, MUFU ex2 or the
+      // FMA-pipe polynomial for the power, packed FADD for the row sum.
+      const float2 c2 = make_float2(c, c), nm2 = make_float2(-m_use, -m_use);
+      float2 ls[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
       for (int cc = 0; cc < 128; cc += 32) {
         uint32_t pk[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          const float x0 = fmaf(sv[cc + 2 * i], c, neg_m);
-          const float x1 = fmaf(sv[cc + 2 * i + 1], c, neg_m);
-          // 6 of every 16 pairs on the FMA pipe, the rest on MUFU (D <= 64: MUFU-bound)
-          const bool poly = C::kPolyExp && (i & 7) < 3;
-          const float p0 = poly ? exp2_poly(x0) : ex2(x0);
-          const float p1 = poly ? exp2_poly(x1) : ex2(x1);
-          ls[i % 4] += p0 + p1;
-          pk[i] = pack_bf16x2(p0, p1);
+          const float2 x = __ffma2_rn(make_float2(sv[cc + 2 * i], sv[cc + 2 * i + 1]), c2, nm2);
+          // a third of the pairs on the FMA pipe when the exp unit co-binds (D <= 64)
+          const bool poly = C::kPolyExp && (i % 3) == 1;
+          const float2 pp = poly ? exp2_poly2(x) : make_float2(ex2(x.x), ex2(x.y));
+          ls[i & 1] = __fadd2_rn(ls[i & 1], pp);
+          pk[i] = pack_bf16x2(pp.x, pp.y);
         }
         tmem_st16(t_lane + colS + cc / 2, pk);
       }
-      l += (ls[0] + ls[1]) + (ls[2] + ls[3]);
+      l += (ls[0].x + ls[0].y) + (ls[1].x + ls[1].y);
       // Lazy rescale of O_t.  PV_t(j-1) has completed: S_t(j), observed
       // complete above, was issued after it by the same thread.
       if (warp_need && j > 0) {
