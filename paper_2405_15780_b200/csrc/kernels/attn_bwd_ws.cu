@@ -37,6 +37,7 @@ struct BwdWsCfg {
   static constexpr uint32_t kColS = 0, kColDP = 128, kColDV = 256, kColDK = 256 + D, kColDQ = 256 + 2 * D;
   static constexpr int kDsBytes = 128 * 128 * 2;
   static constexpr int kStages = 3;                 // Q / dO / (lse, Delta) ring depth
+  static constexpr bool kPolyExp = true;            // 1/4 of exp2 on the FMA pipe
   static constexpr int kStageBytes = 128 * 32 * 4;  // one 32-column fp32 box of the dQ tile
   static constexpr int kLsedBytes = 128 * 8;        // (-lse*log2e, Delta) per query row
   static constexpr int kSmemBytes = 1024 + (2 + 2 * kStages) * G::kTileBytes + 2 * kDsBytes + kStageBytes +
@@ -235,7 +236,10 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_ws_kernel(const __grid_consta
         mbar_wait(&sdp_full[hh], T & 1);
         tc_fence_after();
         uint8_t* atom = sdS + (T & 1) * C::kDsBytes + hh * (128 * 128) + j * 128;
-        const float4* ld4 = reinterpret_cast<const float4*>(s_lsed + s * 128 + 64 * hh);  // (nl0, d0, nl1, d1)
+        const float* tl = reinterpret_cast<const float*>(s_lsed + s * 128);  // [128 -lse*log2e][128 -Delta]
+        const float4* nl4 = reinterpret_cast<const float4*>(tl + 64 * hh);
+        const float4* nd4 = reinterpret_cast<const float4*>(tl + 128 + 64 * hh);
+        const float2 c2 = make_float2(c, c);
 #pragma unroll
         for (int cc = 0; cc < 64; cc += 16) {
           uint32_t rs[16], rd[16];
@@ -244,13 +248,22 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_ws_kernel(const __grid_consta
           tmem_ld_wait();
           uint32_t pk_p[8], pk_ds[8];
 #pragma unroll
-          for (int x = 0; x < 16; x += 2) {
-            const float4 ld = ld4[(cc + x) / 2];
-            const float p0 = ex2(fmaf(__uint_as_float(rs[x + 0]), c, ld.x));
-            const float p1 = ex2(fmaf(__uint_as_float(rs[x + 1]), c, ld.z));
-            pk_p[x / 2] = pack_bf16x2(p0, p1);
-            pk_ds[x / 2] = pack_bf16x2(p0 * (__uint_as_float(rd[x + 0]) - ld.y),
-                                       p1 * (__uint_as_float(rd[x + 1]) - ld.w));
+          for (int x = 0; x < 16; x += 4) {
+            const float4 nl = nl4[(cc + x) / 4];
+            const float4 nd = nd4[(cc + x) / 4];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+              const float2 arg = __ffma2_rn(make_float2(__uint_as_float(rs[x + 2 * u]), __uint_as_float(rs[x + 2 * u + 1])),
+                                            c2, u == 0 ? make_float2(nl.x, nl.y) : make_float2(nl.z, nl.w));
+              // a quarter of the pairs on the FMA-pipe polynomial
+              const bool poly = C::kPolyExp && ((x / 2 + u) & 3) == 1;
+              const float2 pp = poly ? exp2_poly2(arg) : make_float2(ex2(arg.x), ex2(arg.y));
+              const float2 dd = __fadd2_rn(make_float2(__uint_as_float(rd[x + 2 * u]), __uint_as_float(rd[x + 2 * u + 1])),
+                                           u == 0 ? make_float2(nd.x, nd.y) : make_float2(nd.z, nd.w));
+              const float2 ds = __fmul2_rn(pp, dd);
+              pk_p[x / 2 + u] = pack_bf16x2(pp.x, pp.y);
+              pk_ds[x / 2 + u] = pack_bf16x2(ds.x, ds.y);
+            }
           }
           tmem_st8(t_lane + colS + cc / 2, pk_p);
           tmem_st8(t_lane + colDP + cc / 2, pk_ds);

@@ -39,7 +39,7 @@ struct alignas(64) BwdParams {
   int64_t l_sh, l_sb;
   const float* delta; // Delta[b*d_sb + h*d_sh + n*d_sn]
   int64_t d_sn, d_sh, d_sb;
-  const float2* lsed; // [B*heads][N_pad] (-lse*log2(e), Delta), rows >= N = (-inf, 0)  (ws kernel)
+  const float2* lsed; // per head, per 128-row tile: [128 x -lse*log2(e)][128 x -Delta]; rows >= N: (-inf, 0)
   int n;              // sequence length (queries == keys)
   int heads;
   int batch;
@@ -67,7 +67,8 @@ cudaError_t launch_unpack(const void* const* src, void* const* dst, int ntensors
 // dq = bf16(scale * dq_acc), dq_acc [B*heads][N_pad][D] fp32 (N_pad = N rounded up to 128) -> view
 cudaError_t launch_dq_finalize(const float* dq_acc, ViewArg dq, int64_t B, int64_t N, int heads, int D, float scale,
                                cudaStream_t stream);
-// Backward prep: lsed[bh][n] = (-lse*log2(e), Delta) for n < N, (-inf, 0) for N <= n < N_pad.
+// Backward prep: per head bh and 128-row tile, [128 x -lse*log2(e)][128 x -Delta]
+// (rows N <= n < N_pad: -inf, 0).
 cudaError_t launch_bwd_prep(const float* lse, int64_t l_sh, int64_t l_sb, const float* delta, int64_t d_sn,
                             int64_t d_sh, int64_t d_sb, float2* lsed, int64_t B, int heads, int64_t N,
                             cudaStream_t stream);

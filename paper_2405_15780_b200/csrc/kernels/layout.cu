@@ -125,9 +125,15 @@ __global__ void __launch_bounds__(256) bwd_prep_kernel(const float* __restrict__
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
     const int64_t n = i % n_pad, bh = i / n_pad;
     const int64_t b = bh / heads, h = bh % heads;
-    float2 v = make_float2(-INFINITY, 0.f);
-    if (n < N) v = make_float2(-lse[b * l_sb + h * l_sh + n] * 1.4426950408889634f, delta[b * d_sb + h * d_sh + n * d_sn]);
-    lsed[i] = v;
+    float nl = -INFINITY, nd = 0.f;
+    if (n < N) {
+      nl = -lse[b * l_sb + h * l_sh + n] * 1.4426950408889634f;
+      nd = -delta[b * d_sb + h * d_sh + n * d_sn];
+    }
+    // planar per 128-row tile: [128 x (-lse*log2e)][128 x (-Delta)]
+    float* tile = reinterpret_cast<float*>(lsed) + (bh * n_pad + (n / 128) * 128) * 2;
+    tile[n % 128] = nl;
+    tile[128 + n % 128] = nd;
   }
 }
 
