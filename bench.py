@@ -91,15 +91,35 @@ class ClockSampler:
                 self.rows.append(f)
 
     def summary(self, devices):
+        """Median SM clock over samples of the GPUs in use that were under
+        load (power above 40 % of the max seen), and every throttle reason
+        seen on those GPUs."""
         rows = [r for r in getattr(self, "rows", []) if r[0].isdigit() and int(r[0]) in devices]
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
-        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+        pw = [num(r[3]) or 0.0 for r in rows]
+        thr = 0.4 * max(pw) if pw else 0.0
+        loaded = [r for r, w in zip(rows, pw) if w >= thr] or rows
+        sm = [num(r[1]) for r in loaded if num(r[1]) is not None]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": float(rows[0][2]),
-                "reasons": reasons, "samples": len(rows),
-                "power_w_max": max(float(r[3]) for r in rows if r[3].replace(".", "").isdigit())}
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": num(rows[0][2]),
+                "reasons": reasons, "samples": len(rows), "samples_under_load": len(loaded),
+                "power_w_max": max(pw) if pw else None}
+
+
+def devices_in_use(P):
+    """nvidia-smi indices of the GPUs the P local ranks use (local rank r ->
+    CUDA device r, mapped through CUDA_VISIBLE_DEVICES when it is set)."""
+    vis = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+    ids = [int(x) for x in vis.split(",") if x.strip().isdigit()]
+    return set(ids[:P]) if ids else set(range(P))
 
 
 def cpu_baseline(steps=1, n_sample=24576, D=64):
@@ -318,7 +338,7 @@ def main():
             "a2a": {"calls": calls1 - calls0, "bytes_sent_per_rank": a2a_bytes,
                     "GBps": (a2a_bytes / (a2a_ms * 1e-3) / 1e9) if a2a_ms > 0 else None},
             "gpu_launches": launches,
-            "clocks": clk.summary(set(range(torch.cuda.device_count()))),
+            "clocks": clk.summary(devices_in_use(P)),
             "e2e": e2e,
         }
         if P == 1 and not args.no_cpu_baseline:
