@@ -38,8 +38,14 @@ struct FwdCfg {
   static constexpr int kThreads = 384;
   static constexpr int kSmemTiles = (2 + 2 * kStages) * G::kTileBytes;
   static constexpr int kSmemBytes = 1024 + kSmemTiles + 256;
-  static constexpr uint32_t kColS = 0;     // + t*128
-  static constexpr uint32_t kColO = 256;   // + t*D
+  // D <= 64: P gets its own TMEM columns (S0 S1 | P0 P1 | O0 O1 = 512), so the
+  // next S = Q K^T can be issued as soon as the softmax has LOADED S instead of
+  // after P.V consumed P.  D = 128: P aliases S (S0 S1 | O0 O1 = 512).
+  static constexpr bool kSeparateP = D <= 64;
+  static constexpr uint32_t kColS = 0;                          // + t*128
+  static constexpr uint32_t kColP = kSeparateP ? 256 : 0;       // + t*(kSeparateP ? 64 : 128)
+  static constexpr uint32_t kPStride = kSeparateP ? 64 : 128;
+  static constexpr uint32_t kColO = kSeparateP ? 384 : 256;     // + t*D
   static constexpr float kRescaleThreshold = 8.0f;  // log2 units
   static constexpr bool kPolyExp = D <= 64;          // exp unit co-binds only at small D
 };
@@ -62,7 +68,8 @@ __global__ void __launch_bounds__(384, 1) attn_fwd_kernel(const __grid_constant_
   uint64_t* s_full = kv_empty + kStages;  // [2]
   uint64_t* p_full = s_full + 2;          // [2]
   uint64_t* o_done = p_full + 2;          // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
+  uint64_t* s_free = o_done + 2;          // [2] softmax has loaded S_t (kSeparateP)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_free + 2);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -82,6 +89,7 @@ __global__ void __launch_bounds__(384, 1) attn_fwd_kernel(const __grid_constant_
       mbar_init(&s_full[t], 1);
       mbar_init(&p_full[t], 128);
       mbar_init(&o_done[t], 1);
+      mbar_init(&s_free[t], 128);
     }
     fence_mbar_init();
   }
@@ -125,6 +133,46 @@ __global__ void __launch_bounds__(384, 1) attn_fwd_kernel(const __grid_constant_
       const uint32_t sQa = smem_u32(sQ), sKa = smem_u32(sK), sVa = smem_u32(sV);
       mbar_wait(q_full, 0);
       tc_fence_after();
+      auto issue_s = [&](int t, int j) {  // S_t = Q_t K_j^T
+        const uint32_t qt = sQa + t * G::kTileBytes, kt = sKa + (j % kStages) * G::kTileBytes;
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)
+          mma_ss(tbase + C::kColS + t * 128, kmajor_desc<D>(qt, kk), kmajor_desc<D>(kt, kk), idesc_s,
+                 kk > 0 ? 1u : 0u);
+        mma_commit(&s_full[t]);
+      };
+      auto issue_pv = [&](int t, int j) {  // O_t += P_t(j) V_j
+        const uint32_t vt = sVa + (j % kStages) * G::kTileBytes;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          mma_ts(tbase + C::kColO + t * D, tbase + C::kColP + t * C::kPStride + kk * 8, mnmajor_desc<D>(vt, kk),
+                 idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+        mma_commit(&o_done[t]);
+      };
+      if constexpr (C::kSeparateP) {
+        // S_t(j+1) as soon as softmax t has loaded S_t(j); P.V when P is stored.
+        mbar_wait(&k_full[0], 0);
+        tc_fence_after();
+        issue_s(0, 0);
+        issue_s(1, 0);
+        for (int j = 0; j < n_kv; ++j) {
+          if (j + 1 < n_kv) {
+            mbar_wait(&k_full[(j + 1) % kStages], ((j + 1) / kStages) & 1);
+            for (int t = 0; t < 2; ++t) {
+              mbar_wait(&s_free[t], j & 1);
+              tc_fence_after();
+              issue_s(t, j + 1);
+            }
+          }
+          mbar_wait(&v_full[j % kStages], (j / kStages) & 1);
+          for (int t = 0; t < 2; ++t) {
+            mbar_wait(&p_full[t], j & 1);
+            tc_fence_after();
+            issue_pv(t, j);
+          }
+          mma_commit(&kv_empty[j % kStages]);
+        }
+      } else
       for (int j = 0; j <= n_kv; ++j) {
         const int s = j % kStages;
         if (j < n_kv) {
@@ -165,6 +213,7 @@ __global__ void __launch_bounds__(384, 1) attn_fwd_kernel(const __grid_constant_
     const int q_row = q0 + t * 128 + row;      // global query index
     const uint32_t t_lane = tbase + (uint32_t(quad * 32) << 16);
     const uint32_t colS = C::kColS + t * 128, colO = C::kColO + t * D;
+    const uint32_t colP = C::kColP + t * C::kPStride;
     const float c = p.scale_log2;
     float m_use = -INFINITY, l = 0.f;
 
@@ -179,6 +228,10 @@ __global__ void __launch_bounds__(384, 1) attn_fwd_kernel(const __grid_constant_
         tmem_ld_wait();
 #pragma unroll
         for (int i = 0; i < 32; ++i) sv[cc + i] = __uint_as_float(r[i]);
+      }
+      if constexpr (C::kSeparateP) {  // S_t is in registers: the next Q K^T may overwrite it
+        tc_fence_before();
+        mbar_arrive(&s_free[t]);
       }
       const int kv0 = p.kv_begin + j * 128;
       if (kv0 + 128 > p.kv_end) {
@@ -206,6 +259,10 @@ __global__ void __launch_bounds__(384, 1) attn_fwd_kernel(const __grid_constant_
       // FMA-pipe polynomial for the power, packed FADD for the row sum.
       const float2 c2 = make_float2(c, c), nm2 = make_float2(-m_use, -m_use);
       float2 ls[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+      if (C::kSeparateP && j > 0) {  // P_t buffer free: PV_t(j-1) has consumed it
+        mbar_wait(&o_done[t], (j - 1) & 1);
+        tc_fence_after();
+      }
 #pragma unroll
       for (int cc = 0; cc < 128; cc += 32) {
         uint32_t pk[16];
@@ -218,11 +275,10 @@ __global__ void __launch_bounds__(384, 1) attn_fwd_kernel(const __grid_constant_
           ls[i & 1] = __fadd2_rn(ls[i & 1], pp);
           pk[i] = pack_bf16x2(pp.x, pp.y);
         }
-        tmem_st16(t_lane + colS + cc / 2, pk);
+        tmem_st16(t_lane + colP + cc / 2, pk);
       }
       l += (ls[0].x + ls[0].y) + (ls[1].x + ls[1].y);
-      // Lazy rescale of O_t.  PV_t(j-1) has completed: S_t(j), observed
-      // complete above, was issued after it by the same thread.
+      // Lazy rescale of O_t, after PV_t(j-1) has completed (o_done).
       if (warp_need && j > 0) {
         mbar_wait(&o_done[t], (j - 1) & 1);
         tc_fence_after();
