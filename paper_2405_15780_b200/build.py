@@ -75,5 +75,34 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+def build_variant(name: str, defines: dict) -> str:
+    """Tuning aid: build the library with extra -D macros into
+    variants/lib<name>.so (for interleaved A/B timing, scripts/ab.py)."""
+    inc, libdir = _nccl_dirs()
+    objdir = os.path.join(HERE, "build", name)
+    os.makedirs(objdir, exist_ok=True)
+    os.makedirs(os.path.join(HERE, "variants"), exist_ok=True)
+    out = os.path.join(HERE, "variants", f"lib{name}.so")
+    common = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-I", inc, "-I", os.path.join(ROOT, "include"),
+              "-I", CSRC] + [f"-D{k}={v}" for k, v in defines.items()]
+    objs, procs = [], []
+    for src in sources():
+        obj = os.path.join(objdir, os.path.basename(src) + ".o")
+        objs.append(obj)
+        cmd = [NVCC, *ARCH, *common, "-c", src, "-o", obj] + ([] if src.endswith(".cu") else ["-x", "cu"])
+        procs.append((cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
+    for cmd, p in procs:
+        o, _ = p.communicate()
+        if p.returncode != 0:
+            raise RuntimeError("nvcc failed:\n" + " ".join(cmd) + "\n" + o.decode())
+    subprocess.check_call([NVCC, *ARCH, "-shared", "-o", out, *objs, "-L", libdir, "-l:libnccl.so.2",
+                           "-Xlinker", f"-rpath={libdir}", "-lcudart"])
+    return out
+
+
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    if len(sys.argv) > 2 and sys.argv[1] == "--variant":
+        # python build.py --variant NAME KEY=VAL ...
+        print(build_variant(sys.argv[2], dict(a.split("=", 1) for a in sys.argv[3:])))
+    else:
+        print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

@@ -25,6 +25,13 @@
 #include "attn_common.cuh"
 #include "attn_kernels.h"
 
+#ifndef UA_BWD_POLY_MOD
+#define UA_BWD_POLY_MOD 4   // every UA_BWD_POLY_MOD-th exp2 pair on the FMA pipe (0: none)
+#endif
+#ifndef UA_BWD_STAGGER
+#define UA_BWD_STAGGER 16   // query-tile window the persistent CTAs' start tiles are spread over
+#endif
+
 namespace ua {
 
 namespace {
@@ -33,7 +40,7 @@ template <int D>
 struct BwdWsCfg {
   using G = TileGeom<D>;
   static constexpr int kThreads = 512;
-  static constexpr int kStagger = 16;
+  static constexpr int kStagger = UA_BWD_STAGGER;
   static constexpr uint32_t kColS = 0, kColDP = 128, kColDV = 256, kColDK = 256 + D, kColDQ = 256 + 2 * D;
   static constexpr int kDsBytes = 128 * 128 * 2;
   static constexpr int kStages = 3;                 // Q / dO / (lse, Delta) ring depth
@@ -256,7 +263,8 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_ws_kernel(const __grid_consta
               const float2 arg = __ffma2_rn(make_float2(__uint_as_float(rs[x + 2 * u]), __uint_as_float(rs[x + 2 * u + 1])),
                                             c2, u == 0 ? make_float2(nl.x, nl.y) : make_float2(nl.z, nl.w));
               // a quarter of the pairs on the FMA-pipe polynomial
-              const bool poly = C::kPolyExp && ((x / 2 + u) & 3) == 1;
+              const bool poly = C::kPolyExp && UA_BWD_POLY_MOD > 0 &&
+                                ((x / 2 + u) % (UA_BWD_POLY_MOD > 0 ? UA_BWD_POLY_MOD : 1)) == 1;
               const float2 pp = poly ? exp2_poly2(arg) : make_float2(ex2(arg.x), ex2(arg.y));
               const float2 dd = __fadd2_rn(make_float2(__uint_as_float(rd[x + 2 * u]), __uint_as_float(rd[x + 2 * u + 1])),
                                            u == 0 ? make_float2(nd.x, nd.y) : make_float2(nd.z, nd.w));

@@ -27,6 +27,15 @@
 #include "attn_common.cuh"
 #include "attn_kernels.h"
 
+// Tuning knobs (defaults are the shipped configuration; scripts/ab.py builds
+// variants with -D overrides).
+#ifndef UA_FWD_SEP_P
+#define UA_FWD_SEP_P 1      // separate TMEM P buffers when D <= 64
+#endif
+#ifndef UA_FWD_POLY_MOD
+#define UA_FWD_POLY_MOD 3   // every UA_FWD_POLY_MOD-th exp2 pair on the FMA pipe (0: none)
+#endif
+
 namespace ua {
 
 namespace {
@@ -41,7 +50,7 @@ struct FwdCfg {
   // D <= 64: P gets its own TMEM columns (S0 S1 | P0 P1 | O0 O1 = 512), so the
   // next S = Q K^T can be issued as soon as the softmax has LOADED S instead of
   // after P.V consumed P.  D = 128: P aliases S (S0 S1 | O0 O1 = 512).
-  static constexpr bool kSeparateP = D <= 64;
+  static constexpr bool kSeparateP = UA_FWD_SEP_P && D <= 64;
   static constexpr uint32_t kColS = 0;                          // + t*128
   static constexpr uint32_t kColP = kSeparateP ? 256 : 0;       // + t*(kSeparateP ? 64 : 128)
   static constexpr uint32_t kPStride = kSeparateP ? 64 : 128;
@@ -270,7 +279,7 @@ __global__ void __launch_bounds__(384, 1) attn_fwd_kernel(const __grid_constant_
         for (int i = 0; i < 16; ++i) {
           const float2 x = __ffma2_rn(make_float2(sv[cc + 2 * i], sv[cc + 2 * i + 1]), c2, nm2);
           // a third of the pairs on the FMA pipe when the exp unit co-binds (D <= 64)
-          const bool poly = C::kPolyExp && (i % 3) == 1;
+          const bool poly = C::kPolyExp && UA_FWD_POLY_MOD > 0 && (i % (UA_FWD_POLY_MOD > 0 ? UA_FWD_POLY_MOD : 1)) == 1;
           const float2 pp = poly ? exp2_poly2(x) : make_float2(ex2(x.x), ex2(x.y));
           ls[i & 1] = __fadd2_rn(ls[i & 1], pp);
           pk[i] = pack_bf16x2(pp.x, pp.y);
