@@ -141,11 +141,11 @@ Shape make_shape(int64_t B, int64_t N, int H, int D, int P) {
 
 // 4-D map {D, N, heads, B} over a bf16 view with token / head / batch strides (elements).
 ua_status make_map(CUtensorMap* m, const void* base, int D, int64_t N, int heads, int64_t B, int64_t sn, int64_t sh,
-                   int64_t sb) {
+                   int64_t sb, uint32_t box_rows = 128) {
   const uint64_t dims[4] = {uint64_t(D), uint64_t(N), uint64_t(heads), uint64_t(B)};
   const uint64_t strides[3] = {uint64_t(sn) * 2, uint64_t(sh) * 2, uint64_t(sb) * 2};
   const uint32_t box0 = D >= 64 ? 64 : uint32_t(D);
-  if (!ua::make_tmap_bf16_4d(m, base, dims, strides, box0, 128,
+  if (!ua::make_tmap_bf16_4d(m, base, dims, strides, box0, box_rows,
                              D >= 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B))
     return fail(UA_ERR_CUDA, "cuTensorMapEncodeTiled failed (D=%d N=%lld heads=%d)", D, (long long)N, heads);
   return UA_OK;
@@ -262,6 +262,8 @@ ua_status launch_attention_bwd(const void* q, const void* k, const void* v, cons
   UA_TRY(make_map(&p.tm_k, k, D, N, heads, B, sn, sh, sb));
   UA_TRY(make_map(&p.tm_v, v, D, N, heads, B, sn, sh, sb));
   UA_TRY(make_map(&p.tm_do, dout, D, N, heads, B, sn, sh, sb));
+  UA_TRY(make_map(&p.tm_qh, q, D, N, heads, B, sn, sh, sb, 64));
+  UA_TRY(make_map(&p.tm_doh, dout, D, N, heads, B, sn, sh, sb, 64));
   const int64_t n_pad = (N + 127) / 128 * 128;
   if (!ua::make_tmap_f32_2d(&p.tm_dq, dq_acc, uint64_t(D), uint64_t(B * heads * n_pad), 128))
     return fail(UA_ERR_CUDA, "cuTensorMapEncodeTiled failed for dq_acc");

@@ -325,7 +325,7 @@ cudaError_t launch_attn_bwd(const BwdParams& p, int D, int B, int heads, cudaStr
     const char* e = std::getenv("UA_BWD_KERNEL");
     return e != nullptr && std::strcmp(e, "v1") == 0;
   }();
-  if (D <= 64 && !force_v1) return launch_attn_bwd_ws(p, D, stream);
+  if (!force_v1) return launch_attn_bwd_ws(p, D, stream);
   switch (D) {
     case 32: return launch_bwd_impl<32>(p, B, heads, stream);
     case 64: return launch_bwd_impl<64>(p, B, heads, stream);

@@ -1,5 +1,5 @@
-// attn_bwd_ws.cu — persistent, warp-specialised attention backward for D <= 64
-// (sm_100a).
+// attn_bwd_ws.cu — persistent, warp-specialised attention backward (sm_100a),
+// D in {32, 64, 128}.
 //
 // Mathematics as attn_bwd.cu:
 //   P = exp(S - lse), dV += P^T dO, dS = P (dP - Delta), dK += scale dS^T Q,
@@ -10,18 +10,22 @@
 //    (b, h), items in head-major order, CTA c takes items c, c+G, ...  All
 //    CTAs sweep their query tiles at the same rate, so at any moment they
 //    touch a narrow window of Q / dO / dq rows of the same head (L2-resident
-//    even at N = 188K where one head's Q, dO and dq are ~96 MB).  Start tiles
-//    are staggered over a window of kStagger tiles so that only ~G/kStagger
-//    CTAs reduce into the same dq tile at once.
+//    even at N = 188K, where one head's Q, dO and dq are ~96 MB).  Start tiles
+//    are staggered over a window of kStagger tiles so only ~G/kStagger CTAs
+//    reduce into the same dq tile at once.
 //  * 16 warps: 0 TMA producer, 1 tcgen05.mma issuer, 4-7 elementwise for the
-//    even 64-query half, 8-11 for the odd half, 12-15 dQ drain.  Each query
-//    tile's halves have separate TMEM S^T / dP^T buffers, so the two
-//    elementwise warpgroups and the tensor core work on different halves at
-//    the same time.
-//  * dQ: TMEM -> swizzled fp32 smem tile -> TMA tensor reduce-add
+//    even 64-query half of each tile, 8-11 for the odd half, 12-15 dQ drain.
+//    The halves have separate TMEM S^T / dP^T buffers, so the two elementwise
+//    warpgroups and the tensor core work on different halves concurrently.
+//  * Q / dO / (lse, Delta) arrive in a ring of 64-query half-tile slots; a
+//    slot is released as soon as that half's dV / dK GEMMs are done.
+//  * dQ: TMEM -> swizzled fp32 smem box -> TMA tensor reduce-add
 //    (cp.reduce.async.bulk.tensor .add) into dq_acc.
-// TMEM: S^T[h] [64h, +64)  dP^T[h] [128+64h, +64)  dV [256, +D)  dK [256+D, +D)
-//       dQ [256+2D, +D).
+//  * K, V stay in smem for the whole item (A operands of S^T, dP^T; B of dQ).
+// TMEM (512 columns):  S^T[h] [64h, +64)  dP^T[h] [128+64h, +64)  dV [256, +D)
+//   dK [256+D, +D)  dQ [256+2D, +D) for D <= 64.  D = 128 has no room for dQ:
+//   it aliases dP^T [128, 256) and the next tile's dP^T GEMMs wait for the dQ
+//   drain (the S^T GEMMs of the next tile run meanwhile).
 #include "attn_common.cuh"
 #include "attn_kernels.h"
 
@@ -41,68 +45,76 @@ struct BwdWsCfg {
   using G = TileGeom<D>;
   static constexpr int kThreads = 512;
   static constexpr int kStagger = UA_BWD_STAGGER;
-  static constexpr uint32_t kColS = 0, kColDP = 128, kColDV = 256, kColDK = 256 + D, kColDQ = 256 + 2 * D;
+  static constexpr bool kAliasDq = (256 + 3 * D) > 512;
+  static constexpr uint32_t kColS = 0, kColDP = 128, kColDV = 256, kColDK = 256 + D;
+  static constexpr uint32_t kColDQ = kAliasDq ? 128 : 256 + 2 * D;
+  static constexpr int kHalfBytes = 64 * D * 2;               // one [64][D] bf16 half tile
+  static constexpr int kSlots = D == 128 ? 3 : 6;              // half-tile ring depth
+  static constexpr int kSlotBytes = 2 * kHalfBytes;            // Q_h + dO_h
+  static constexpr int kNumDs = kAliasDq ? 1 : 2;              // dS^T smem buffers
   static constexpr int kDsBytes = 128 * 128 * 2;
-  static constexpr int kStages = 3;                 // Q / dO / (lse, Delta) ring depth
-  static constexpr bool kPolyExp = true;            // 1/4 of exp2 on the FMA pipe
-  static constexpr int kStageBytes = 128 * 32 * 4;  // one 32-column fp32 box of the dQ tile
-  static constexpr int kLsedBytes = 128 * 8;        // (-lse*log2e, Delta) per query row
-  static constexpr int kSmemBytes = 1024 + (2 + 2 * kStages) * G::kTileBytes + 2 * kDsBytes + kStageBytes +
-                                    kStages * kLsedBytes + 256;
-  static_assert(256 + 3 * D <= 512, "TMEM budget");
+  static constexpr int kStageBoxes = D == 128 ? 2 : 1;         // 16 KB fp32 staging boxes for dQ
+  static constexpr int kBoxBytes = 128 * 32 * 4;
+  static constexpr int kLsedBytes = 128 * 4;                   // per slot: 64 x -lse*log2e, 64 x -Delta
+  static constexpr bool kPolyExp = UA_BWD_POLY_MOD > 0;
+  static constexpr int kSmemBytes = 1024 + 2 * G::kTileBytes + kSlots * kSlotBytes + kNumDs * kDsBytes +
+                                    kStageBoxes * kBoxBytes + kSlots * kLsedBytes + 256;
+  static_assert(kSmemBytes <= 232448, "smem budget");
 };
 
 template <int D>
 __global__ void __launch_bounds__(512, 1) attn_bwd_ws_kernel(const __grid_constant__ BwdParams p) {
   using C = BwdWsCfg<D>;
   using G = TileGeom<D>;
+  constexpr int kSl = C::kSlots;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sK = smem;
   uint8_t* sV = sK + G::kTileBytes;
-  constexpr int kS = C::kStages;
-  uint8_t* sQ = sV + G::kTileBytes;               // [kS]
-  uint8_t* sdO = sQ + kS * G::kTileBytes;         // [kS]
-  uint8_t* sdS = sdO + kS * G::kTileBytes;        // [2] dS^T [128 keys][128 q] bf16 (2 SW128 atoms)
-  uint8_t* sStage = sdS + 2 * C::kDsBytes;        // one SW128 box [128][32] fp32 of the dQ tile
-  float2* s_lsed = reinterpret_cast<float2*>(sStage + C::kStageBytes);  // [kS][128] (-lse*log2e, Delta)
-  uint64_t* bars = reinterpret_cast<uint64_t*>(s_lsed + kS * 128);
+  uint8_t* sSlots = sV + G::kTileBytes;                        // [kSl] { Q_h, dO_h }
+  uint8_t* sdS = sSlots + kSl * C::kSlotBytes;                 // [kNumDs] dS^T [128 keys][128 q], 2 SW128 atoms
+  uint8_t* sStage = sdS + C::kNumDs * C::kDsBytes;             // [kStageBoxes] fp32 [128][32] SW128
+  float* sLsed = reinterpret_cast<float*>(sStage + C::kStageBoxes * C::kBoxBytes);  // [kSl][128]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sLsed + kSl * 128);
   uint64_t* kv_full = bars + 0;
   uint64_t* kv_empty = bars + 1;
-  uint64_t* sdp_full = bars + 2;      // [2] per half
-  uint64_t* ds_ready = bars + 4;      // [2] per half
-  uint64_t* ds_free = bars + 6;       // [2] per dS buffer
-  uint64_t* dq_full = bars + 8;
-  uint64_t* dq_empty = bars + 9;
-  uint64_t* acc_full = bars + 10;
-  uint64_t* acc_free = bars + 11;
-  uint64_t* qdo_full = bars + 12;     // [kS]
-  uint64_t* qdo_empty = qdo_full + kS;  // [kS]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(qdo_empty + kS);
+  uint64_t* dq_full = bars + 2;
+  uint64_t* dq_empty = bars + 3;
+  uint64_t* acc_full = bars + 4;
+  uint64_t* acc_free = bars + 5;
+  uint64_t* sdp_full = bars + 6;      // [2] per half
+  uint64_t* ds_ready = bars + 8;      // [2] per half
+  uint64_t* ds_free = bars + 10;      // [kNumDs]
+  uint64_t* slot_full = bars + 12;    // [kSl]
+  uint64_t* slot_empty = slot_full + kSl;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(slot_empty + kSl);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
   const int n_q = (p.n + 127) / 128;
+  const int n_pad = n_q * 128;
   const int n_kt = n_q;
   const int n_items = p.batch * p.heads * n_kt;
   const int start = int((int64_t(blockIdx.x) * C::kStagger) / gridDim.x) % n_q;
+  auto qslot = [&](int s) { return sSlots + s * C::kSlotBytes; };
+  auto doslot = [&](int s) { return sSlots + s * C::kSlotBytes + C::kHalfBytes; };
 
   if (threadIdx.x == 0) {
     mbar_init(kv_full, 1);
     mbar_init(kv_empty, 1);
-    for (int s = 0; s < kS; ++s) {
-      mbar_init(&qdo_full[s], 1);
-      mbar_init(&qdo_empty[s], 1);
-    }
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(&sdp_full[s], 1);
-      mbar_init(&ds_ready[s], 128);
-      mbar_init(&ds_free[s], 1);
-    }
     mbar_init(dq_full, 1);
     mbar_init(dq_empty, 128);
     mbar_init(acc_full, 1);
     mbar_init(acc_free, 256);
+    for (int h = 0; h < 2; ++h) {
+      mbar_init(&sdp_full[h], 1);
+      mbar_init(&ds_ready[h], 128);
+    }
+    for (int i = 0; i < C::kNumDs; ++i) mbar_init(&ds_free[i], 1);
+    for (int s = 0; s < kSl; ++s) {
+      mbar_init(&slot_full[s], 1);
+      mbar_init(&slot_empty[s], 1);
+    }
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc<512>(tmem_slot);
@@ -114,14 +126,11 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_ws_kernel(const __grid_consta
   if (warp == 0) {
     // ------------------------------------------------------------ producer
     if (lane == 0) {
-      tma_prefetch_desc(&p.tm_q);
+      tma_prefetch_desc(&p.tm_qh);
       tma_prefetch_desc(&p.tm_k);
       tma_prefetch_desc(&p.tm_v);
-      tma_prefetch_desc(&p.tm_do);
-    }
-    if (lane == 0) {
+      tma_prefetch_desc(&p.tm_doh);
       int T = 0, it = 0;
-      const int n_pad = n_q * 128;
       for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
         const int kt = item % n_kt, bh = item / n_kt;
         const int b = bh / p.heads, h = bh % p.heads;
@@ -131,19 +140,23 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_ws_kernel(const __grid_consta
           tma_load_4d(sK + a * G::kAtomBytes, &p.tm_k, kv_full, a * G::kAtomCols, kt * 128, h, b, kEvictFirst);
           tma_load_4d(sV + a * G::kAtomBytes, &p.tm_v, kv_full, a * G::kAtomCols, kt * 128, h, b, kEvictFirst);
         }
-        const float2* lsed_bh = p.lsed + int64_t(bh) * n_pad;
+        const float* lsed_bh = reinterpret_cast<const float*>(p.lsed) + int64_t(bh) * n_pad * 2;
         for (int t = 0; t < n_q; ++t, ++T) {
-          const int s = T % kS;
           const int tile = (start + t) % n_q;
-          if (T >= kS) mbar_wait(&qdo_empty[s], ((T / kS) & 1) ^ 1);
-          mbar_arrive_expect_tx(&qdo_full[s], 2 * G::kTileBytes + C::kLsedBytes);
-          for (int a = 0; a < G::kAtoms; ++a) {
-            tma_load_4d(sQ + s * G::kTileBytes + a * G::kAtomBytes, &p.tm_q, &qdo_full[s], a * G::kAtomCols,
-                        tile * 128, h, b, kEvictLast);
-            tma_load_4d(sdO + s * G::kTileBytes + a * G::kAtomBytes, &p.tm_do, &qdo_full[s], a * G::kAtomCols,
-                        tile * 128, h, b, kEvictLast);
+          const float* lsed_tile = lsed_bh + int64_t(tile) * 256;  // [128 nl][128 nd]
+          for (int hh = 0; hh < 2; ++hh) {
+            const int U = 2 * T + hh, s = U % kSl;
+            if (U >= kSl) mbar_wait(&slot_empty[s], ((U / kSl) & 1) ^ 1);
+            mbar_arrive_expect_tx(&slot_full[s], C::kSlotBytes + C::kLsedBytes);
+            for (int a = 0; a < G::kAtoms; ++a) {
+              tma_load_4d(qslot(s) + a * 64 * G::kSw, &p.tm_qh, &slot_full[s], a * G::kAtomCols, tile * 128 + 64 * hh,
+                          h, b, kEvictLast);
+              tma_load_4d(doslot(s) + a * 64 * G::kSw, &p.tm_doh, &slot_full[s], a * G::kAtomCols,
+                          tile * 128 + 64 * hh, h, b, kEvictLast);
+            }
+            bulk_load(sLsed + s * 128, lsed_tile + 64 * hh, 256, &slot_full[s]);
+            bulk_load(sLsed + s * 128 + 64, lsed_tile + 128 + 64 * hh, 256, &slot_full[s]);
           }
-          bulk_load(s_lsed + s * 128, lsed_bh + tile * 128, C::kLsedBytes, &qdo_full[s]);
         }
       }
     }
@@ -153,69 +166,88 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_ws_kernel(const __grid_consta
       const uint32_t idesc_s = idesc_bf16_f32(128, 64, false, false);  // S^T, dP^T half: N = 64 queries
       const uint32_t idesc_g = idesc_bf16_f32(128, D, false, true);    // dV, dK: A = TMEM, B MN-major
       const uint32_t idesc_q = idesc_bf16_f32(128, D, true, true);     // dQ: A, B MN-major
-      const uint32_t sKa = smem_u32(sK), sVa = smem_u32(sV), sQa = smem_u32(sQ), sdOa = smem_u32(sdO);
-      const uint32_t sdSa = smem_u32(sdS);
-      auto issue_sdp = [&](int T, int hh) {
-        const int s = T % kS;
-        const uint32_t qt = sQa + s * G::kTileBytes + 64 * hh * G::kSw;
-        const uint32_t dot = sdOa + s * G::kTileBytes + 64 * hh * G::kSw;
+      const uint32_t sKa = smem_u32(sK), sVa = smem_u32(sV), sSa = smem_u32(sSlots), sdSa = smem_u32(sdS);
+      auto q_at = [&](int U) { return sSa + (U % kSl) * C::kSlotBytes; };
+      auto do_at = [&](int U) { return sSa + (U % kSl) * C::kSlotBytes + C::kHalfBytes; };
+      auto wait_slot = [&](int U) {
+        mbar_wait(&slot_full[U % kSl], (U / kSl) & 1);
+        tc_fence_after();
+      };
+      auto issue_s = [&](int T, int hh) {   // S^T[hh] = K Q_h^T
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk)
-          mma_ss(tbase + C::kColS + 64 * hh, kmajor_desc<D>(sKa, kk), kmajor_desc<D>(qt, kk), idesc_s,
-                 kk > 0 ? 1u : 0u);
+          mma_ss(tbase + C::kColS + 64 * hh, kmajor_desc_r<D, 128>(sKa, kk), kmajor_desc_r<D, 64>(q_at(2 * T + hh), kk),
+                 idesc_s, kk > 0 ? 1u : 0u);
+      };
+      auto issue_dp = [&](int T, int hh) {  // dP^T[hh] = V dO_h^T
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk)
-          mma_ss(tbase + C::kColDP + 64 * hh, kmajor_desc<D>(sVa, kk), kmajor_desc<D>(dot, kk), idesc_s,
-                 kk > 0 ? 1u : 0u);
+          mma_ss(tbase + C::kColDP + 64 * hh, kmajor_desc_r<D, 128>(sVa, kk),
+                 kmajor_desc_r<D, 64>(do_at(2 * T + hh), kk), idesc_s, kk > 0 ? 1u : 0u);
         mma_commit(&sdp_full[hh]);
       };
       int T = 0, it = 0;
       for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
         mbar_wait(kv_full, it & 1);
-        mbar_wait(&qdo_full[T % kS], (T / kS) & 1);
         tc_fence_after();
-        issue_sdp(T, 0);
-        issue_sdp(T, 1);
+        // first tile of the item
+        wait_slot(2 * T);
+        issue_s(T, 0);
+        if constexpr (!C::kAliasDq) issue_dp(T, 0);
+        wait_slot(2 * T + 1);
+        issue_s(T, 1);
+        if constexpr (C::kAliasDq) {
+          if (T > 0) {
+            mbar_wait(dq_empty, (T - 1) & 1);
+            tc_fence_after();
+          }
+          issue_dp(T, 0);
+        }
+        issue_dp(T, 1);
         if (it > 0) {
           mbar_wait(acc_free, (it - 1) & 1);  // previous item's dV / dK drained
           tc_fence_after();
         }
         for (int t = 0; t < n_q; ++t, ++T) {
-          const int s = T % kS;
-          const uint32_t qt = sQa + s * G::kTileBytes, dot = sdOa + s * G::kTileBytes;
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {
+            const int U = 2 * T + hh;
             mbar_wait(&ds_ready[hh], T & 1);
             tc_fence_after();
             const uint32_t acc = (t > 0 || hh > 0) ? 1u : 0u;
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk)
-              mma_ts(tbase + C::kColDV, tbase + C::kColS + 64 * hh + kk * 8, mnmajor_desc<D>(dot, 4 * hh + kk),
+              mma_ts(tbase + C::kColDV, tbase + C::kColS + 64 * hh + kk * 8, mnmajor_desc_r<D, 64>(do_at(U), kk),
                      idesc_g, (acc || kk > 0) ? 1u : 0u);
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk)
-              mma_ts(tbase + C::kColDK, tbase + C::kColDP + 64 * hh + kk * 8, mnmajor_desc<D>(qt, 4 * hh + kk),
+              mma_ts(tbase + C::kColDK, tbase + C::kColDP + 64 * hh + kk * 8, mnmajor_desc_r<D, 64>(q_at(U), kk),
                      idesc_g, (acc || kk > 0) ? 1u : 0u);
-            if (hh == 1) {
-              if (T > 0) {
+            mma_commit(&slot_empty[U % kSl]);
+            if (hh == 1) {  // dQ(T) = dS K
+              if (!C::kAliasDq && T > 0) {
                 mbar_wait(dq_empty, (T - 1) & 1);
                 tc_fence_after();
               }
-              const uint32_t ds = sdSa + (T & 1) * C::kDsBytes;
+              const uint32_t ds = sdSa + (T % C::kNumDs) * C::kDsBytes;
 #pragma unroll
               for (int kk = 0; kk < 8; ++kk)
-                mma_ss(tbase + C::kColDQ, mnmajor_desc<128>(ds, kk), mnmajor_desc<D>(sKa, kk), idesc_q,
+                mma_ss(tbase + C::kColDQ, mnmajor_desc_r<128, 128>(ds, kk), mnmajor_desc_r<D, 128>(sKa, kk), idesc_q,
                        kk > 0 ? 1u : 0u);
               mma_commit(dq_full);
-              mma_commit(&ds_free[T & 1]);
-              mma_commit(&qdo_empty[s]);
+              mma_commit(&ds_free[T % C::kNumDs]);
             }
-            if (t + 1 < n_q) {
-              if (hh == 0) {
-                mbar_wait(&qdo_full[(T + 1) % kS], ((T + 1) / kS) & 1);
+            if (t + 1 < n_q) {  // next tile, this half
+              wait_slot(2 * (T + 1) + hh);
+              issue_s(T + 1, hh);
+              if constexpr (!C::kAliasDq) {
+                issue_dp(T + 1, hh);
+              } else if (hh == 1) {  // dP^T of the next tile overwrites the dQ region
+                mbar_wait(dq_empty, T & 1);
                 tc_fence_after();
+                issue_dp(T + 1, 0);
+                issue_dp(T + 1, 1);
               }
-              issue_sdp(T + 1, hh);
             }
           }
         }
@@ -232,21 +264,20 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_ws_kernel(const __grid_consta
     const uint32_t t_lane = tbase + (uint32_t(quad * 32) << 16);
     const uint32_t colS = C::kColS + 64 * hh, colDP = C::kColDP + 64 * hh;
     const float c = p.scale_log2;
+    const float2 c2 = make_float2(c, c);
     int T = 0, it = 0;
     for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
       const int kt = item % n_kt, bh = item / n_kt;
       const int b = bh / p.heads, h = bh % p.heads;
       for (int t = 0; t < n_q; ++t, ++T) {
-        const int s = T % kS;
-        mbar_wait(&qdo_full[s], (T / kS) & 1);                       // (lse, Delta) landed
-        if (T >= 2) mbar_wait(&ds_free[T & 1], ((T >> 1) & 1) ^ 1);  // dS buffer consumed by dQ(T-2)
+        const int U = 2 * T + hh, s = U % kSl;
+        mbar_wait(&slot_full[s], (U / kSl) & 1);  // (lse, Delta) of this half landed
+        if (T >= C::kNumDs) mbar_wait(&ds_free[T % C::kNumDs], ((T / C::kNumDs) & 1) ^ 1);
         mbar_wait(&sdp_full[hh], T & 1);
         tc_fence_after();
-        uint8_t* atom = sdS + (T & 1) * C::kDsBytes + hh * (128 * 128) + j * 128;
-        const float* tl = reinterpret_cast<const float*>(s_lsed + s * 128);  // [128 -lse*log2e][128 -Delta]
-        const float4* nl4 = reinterpret_cast<const float4*>(tl + 64 * hh);
-        const float4* nd4 = reinterpret_cast<const float4*>(tl + 128 + 64 * hh);
-        const float2 c2 = make_float2(c, c);
+        uint8_t* atom = sdS + (T % C::kNumDs) * C::kDsBytes + hh * (128 * 128) + j * 128;
+        const float4* nl4 = reinterpret_cast<const float4*>(sLsed + s * 128);
+        const float4* nd4 = reinterpret_cast<const float4*>(sLsed + s * 128 + 64);
 #pragma unroll
         for (int cc = 0; cc < 64; cc += 16) {
           uint32_t rs[16], rd[16];
@@ -262,9 +293,7 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_ws_kernel(const __grid_consta
             for (int u = 0; u < 2; ++u) {
               const float2 arg = __ffma2_rn(make_float2(__uint_as_float(rs[x + 2 * u]), __uint_as_float(rs[x + 2 * u + 1])),
                                             c2, u == 0 ? make_float2(nl.x, nl.y) : make_float2(nl.z, nl.w));
-              // a quarter of the pairs on the FMA-pipe polynomial
-              const bool poly = C::kPolyExp && UA_BWD_POLY_MOD > 0 &&
-                                ((x / 2 + u) % (UA_BWD_POLY_MOD > 0 ? UA_BWD_POLY_MOD : 1)) == 1;
+              const bool poly = C::kPolyExp && ((x / 2 + u) % (UA_BWD_POLY_MOD > 0 ? UA_BWD_POLY_MOD : 1)) == 1;
               const float2 pp = poly ? exp2_poly2(arg) : make_float2(ex2(arg.x), ex2(arg.y));
               const float2 dd = __fadd2_rn(make_float2(__uint_as_float(rd[x + 2 * u]), __uint_as_float(rd[x + 2 * u + 1])),
                                            u == 0 ? make_float2(nd.x, nd.y) : make_float2(nd.z, nd.w));
@@ -319,7 +348,8 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_ws_kernel(const __grid_consta
     const int r = quad * 32 + lane;  // query row within the tile
     const bool leader = threadIdx.x == 384;
     const uint32_t t_lane = tbase + (uint32_t(quad * 32) << 16);
-    const int n_pad = n_q * 128;
+    constexpr int kCols = D == 128 ? 64 : D;   // columns held in registers per round
+    constexpr int kRounds = D / kCols;
     int T = 0;
     for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
       const int bh = item / n_kt;
@@ -327,32 +357,45 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_ws_kernel(const __grid_consta
         const int tile = (start + t) % n_q;
         mbar_wait(dq_full, T & 1);
         tc_fence_after();
-        float acc[D];
 #pragma unroll
-        for (int cc = 0; cc < D; cc += 16) {
-          uint32_t x[16];
-          tmem_ld16(t_lane + C::kColDQ + cc, x);
-          tmem_ld_wait();
+        for (int rd = 0; rd < kRounds; ++rd) {
+          float acc[kCols];
 #pragma unroll
-          for (int e = 0; e < 16; ++e) acc[cc + e] = __uint_as_float(x[e]);
-        }
-        tc_fence_before();
-        mbar_arrive(dq_empty);
-        uint8_t* srow = sStage + r * 128;
+          for (int cc = 0; cc < kCols; cc += 16) {
+            uint32_t x[16];
+            tmem_ld16(t_lane + C::kColDQ + rd * kCols + cc, x);
+            tmem_ld_wait();
 #pragma unroll
-        for (int cb = 0; cb < D / 32; ++cb) {
-          if (leader) bulk_wait_read<0>();   // previous reduction has read the staging box
-          named_bar_sync(1, 128);
+            for (int e = 0; e < 16; ++e) acc[cc + e] = __uint_as_float(x[e]);
+          }
+          if (rd == kRounds - 1) {
+            tc_fence_before();
+            mbar_arrive(dq_empty);
+          }
+          // kCols / 32 boxes through kStageBoxes staging boxes
 #pragma unroll
-          for (int q4 = 0; q4 < 8; ++q4)
-            *reinterpret_cast<float4*>(srow + ((q4 ^ (r & 7)) * 16)) =
-                make_float4(acc[32 * cb + 4 * q4], acc[32 * cb + 4 * q4 + 1], acc[32 * cb + 4 * q4 + 2],
-                            acc[32 * cb + 4 * q4 + 3]);
-          fence_proxy_async_smem();
-          named_bar_sync(1, 128);
-          if (leader) {
-            tma_reduce_add_2d(&p.tm_dq, sStage, 32 * cb, bh * n_pad + tile * 128);
-            bulk_commit();
+          for (int cb0 = 0; cb0 < kCols / 32; cb0 += C::kStageBoxes) {
+            if (leader) bulk_wait_read<0>();   // previous reduction has read the staging boxes
+            named_bar_sync(1, 128);
+#pragma unroll
+            for (int sb = 0; sb < C::kStageBoxes; ++sb) {
+              uint8_t* srow = sStage + sb * C::kBoxBytes + r * 128;
+#pragma unroll
+              for (int q4 = 0; q4 < 8; ++q4) {
+                const int e = 32 * (cb0 + sb) + 4 * q4;
+                *reinterpret_cast<float4*>(srow + ((q4 ^ (r & 7)) * 16)) =
+                    make_float4(acc[e], acc[e + 1], acc[e + 2], acc[e + 3]);
+              }
+            }
+            fence_proxy_async_smem();
+            named_bar_sync(1, 128);
+            if (leader) {
+#pragma unroll
+              for (int sb = 0; sb < C::kStageBoxes; ++sb)
+                tma_reduce_add_2d(&p.tm_dq, sStage + sb * C::kBoxBytes, rd * kCols + 32 * (cb0 + sb),
+                                  bh * n_pad + tile * 128);
+              bulk_commit();
+            }
           }
         }
       }
@@ -389,6 +432,7 @@ cudaError_t launch_attn_bwd_ws(const BwdParams& p, int D, cudaStream_t stream) {
   switch (D) {
     case 32: return launch_bwd_ws_impl<32>(p, stream);
     case 64: return launch_bwd_ws_impl<64>(p, stream);
+    case 128: return launch_bwd_ws_impl<128>(p, stream);
     default: return cudaErrorInvalidValue;
   }
 }

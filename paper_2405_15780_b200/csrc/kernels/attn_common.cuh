@@ -45,6 +45,19 @@ __device__ __forceinline__ uint64_t mnmajor_desc(uint32_t tile, int kk) {
   return sdesc(tile + kk * 16 * G::kSw, G::kAtomBytes, G::kSBO, G::kLayout);
 }
 
+// Same two descriptors for a tile of ROWS rows (atoms of ROWS x kSw bytes).
+template <int D, int ROWS>
+__device__ __forceinline__ uint64_t kmajor_desc_r(uint32_t tile, int kk) {
+  using G = TileGeom<D>;
+  uint32_t off = ((kk * 16) / G::kAtomCols) * (ROWS * G::kSw) + ((kk * 32) % G::kSw);
+  return sdesc(tile + off, 16, G::kSBO, G::kLayout);
+}
+template <int D, int ROWS>
+__device__ __forceinline__ uint64_t mnmajor_desc_r(uint32_t tile, int kk) {
+  using G = TileGeom<D>;
+  return sdesc(tile + kk * 16 * G::kSw, ROWS * G::kSw, G::kSBO, G::kLayout);
+}
+
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 

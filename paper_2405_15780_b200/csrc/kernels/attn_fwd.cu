@@ -30,7 +30,7 @@
 // Tuning knobs (defaults are the shipped configuration; scripts/ab.py builds
 // variants with -D overrides).
 #ifndef UA_FWD_SEP_P
-#define UA_FWD_SEP_P 1      // separate TMEM P buffers when D <= 64
+#define UA_FWD_SEP_P 0      // separate TMEM P buffers when D <= 64 (A/B: slower, kept as an option)
 #endif
 #ifndef UA_FWD_POLY_MOD
 #define UA_FWD_POLY_MOD 3   // every UA_FWD_POLY_MOD-th exp2 pair on the FMA pipe (0: none)

@@ -33,6 +33,8 @@ struct alignas(64) BwdParams {
   CUtensorMap tm_v;
   CUtensorMap tm_do;
   CUtensorMap tm_dq;  // fp32 2-D {D, B*heads*N_pad} over dq_acc, box {32, 128}, SW128 (reduce-add target)
+  CUtensorMap tm_qh;  // Q / dO with 64-row boxes (half-tile ring of the ws kernel)
+  CUtensorMap tm_doh;
   ViewArg dk, dv;     // bf16 outputs
   float* dq_acc;      // fp32 [B*heads][N_pad][D] accumulator, N_pad = ceil(N/128)*128 (zeroed by caller)
   const float* lse;   // lse[b*l_sb + h*l_sh + n]
