@@ -32,6 +32,9 @@
 #ifndef UA_BWD_POLY_MOD
 #define UA_BWD_POLY_MOD 4   // every UA_BWD_POLY_MOD-th exp2 pair on the FMA pipe (0: none)
 #endif
+#ifndef UA_BWD_KV_TMEM
+#define UA_BWD_KV_TMEM 1    // D <= 64: K, V copied into TMEM once per work item (TS MMAs)
+#endif
 #ifndef UA_BWD_STAGGER
 #define UA_BWD_STAGGER 16   // query-tile window the persistent CTAs' start tiles are spread over
 #endif
@@ -48,6 +51,10 @@ struct BwdWsCfg {
   static constexpr bool kAliasDq = (256 + 3 * D) > 512;
   static constexpr uint32_t kColS = 0, kColDP = 128, kColDV = 256, kColDK = 256 + D;
   static constexpr uint32_t kColDQ = kAliasDq ? 128 : 256 + 2 * D;
+  // D <= 64: K and V also live in TMEM (bf16 pairs, D/2 columns each) as the A
+  // operands of S^T = K Q^T and dP^T = V dO^T, taking those reads off the smem port.
+  static constexpr bool kKvTmem = UA_BWD_KV_TMEM && D <= 64;
+  static constexpr uint32_t kColK = 256 + 3 * D, kColV = 256 + 3 * D + D / 2;
   static constexpr int kHalfBytes = 64 * D * 2;               // one [64][D] bf16 half tile
   static constexpr int kSlots = D == 128 ? 3 : 6;              // half-tile ring depth
   static constexpr int kSlotBytes = 2 * kHalfBytes;            // Q_h + dO_h
@@ -87,7 +94,8 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_ws_kernel(const __grid_consta
   uint64_t* ds_free = bars + 10;      // [kNumDs]
   uint64_t* slot_full = bars + 12;    // [kSl]
   uint64_t* slot_empty = slot_full + kSl;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(slot_empty + kSl);
+  uint64_t* kv_tmem = slot_empty + kSl;  // K, V copied into TMEM for this item
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(kv_tmem + 1);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -106,6 +114,7 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_ws_kernel(const __grid_consta
     mbar_init(dq_empty, 128);
     mbar_init(acc_full, 1);
     mbar_init(acc_free, 256);
+    mbar_init(kv_tmem, 128);
     for (int h = 0; h < 2; ++h) {
       mbar_init(&sdp_full[h], 1);
       mbar_init(&ds_ready[h], 128);
@@ -175,20 +184,30 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_ws_kernel(const __grid_consta
       };
       auto issue_s = [&](int T, int hh) {   // S^T[hh] = K Q_h^T
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk)
-          mma_ss(tbase + C::kColS + 64 * hh, kmajor_desc_r<D, 128>(sKa, kk), kmajor_desc_r<D, 64>(q_at(2 * T + hh), kk),
-                 idesc_s, kk > 0 ? 1u : 0u);
+        for (int kk = 0; kk < D / 16; ++kk) {
+          if constexpr (C::kKvTmem)
+            mma_ts(tbase + C::kColS + 64 * hh, tbase + C::kColK + kk * 8, kmajor_desc_r<D, 64>(q_at(2 * T + hh), kk),
+                   idesc_s, kk > 0 ? 1u : 0u);
+          else
+            mma_ss(tbase + C::kColS + 64 * hh, kmajor_desc_r<D, 128>(sKa, kk),
+                   kmajor_desc_r<D, 64>(q_at(2 * T + hh), kk), idesc_s, kk > 0 ? 1u : 0u);
+        }
       };
       auto issue_dp = [&](int T, int hh) {  // dP^T[hh] = V dO_h^T
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk)
-          mma_ss(tbase + C::kColDP + 64 * hh, kmajor_desc_r<D, 128>(sVa, kk),
-                 kmajor_desc_r<D, 64>(do_at(2 * T + hh), kk), idesc_s, kk > 0 ? 1u : 0u);
+        for (int kk = 0; kk < D / 16; ++kk) {
+          if constexpr (C::kKvTmem)
+            mma_ts(tbase + C::kColDP + 64 * hh, tbase + C::kColV + kk * 8,
+                   kmajor_desc_r<D, 64>(do_at(2 * T + hh), kk), idesc_s, kk > 0 ? 1u : 0u);
+          else
+            mma_ss(tbase + C::kColDP + 64 * hh, kmajor_desc_r<D, 128>(sVa, kk),
+                   kmajor_desc_r<D, 64>(do_at(2 * T + hh), kk), idesc_s, kk > 0 ? 1u : 0u);
+        }
         mma_commit(&sdp_full[hh]);
       };
       int T = 0, it = 0;
       for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
-        mbar_wait(kv_full, it & 1);
+        mbar_wait(C::kKvTmem ? kv_tmem : kv_full, it & 1);
         tc_fence_after();
         // first tile of the item
         wait_slot(2 * T);
@@ -269,6 +288,31 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_ws_kernel(const __grid_consta
     for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
       const int kt = item % n_kt, bh = item / n_kt;
       const int b = bh / p.heads, h = bh % p.heads;
+      if constexpr (C::kKvTmem) {
+        if (hh == 0) {  // copy this item's K, V rows (row j per thread) into TMEM as bf16 pairs
+          mbar_wait(kv_full, it & 1);
+          const uint32_t sw = (uint32_t(j * G::kSw) >> 7) & uint32_t(G::kSw / 16 - 1);
+          uint32_t rk[D / 2], rv[D / 2];
+#pragma unroll
+          for (int ch = 0; ch < D / 8; ++ch) {
+            const uint32_t off = j * G::kSw + ((ch ^ sw) * 16);
+            const uint4 k4 = *reinterpret_cast<const uint4*>(sK + off);
+            const uint4 v4 = *reinterpret_cast<const uint4*>(sV + off);
+            rk[4 * ch] = k4.x; rk[4 * ch + 1] = k4.y; rk[4 * ch + 2] = k4.z; rk[4 * ch + 3] = k4.w;
+            rv[4 * ch] = v4.x; rv[4 * ch + 1] = v4.y; rv[4 * ch + 2] = v4.z; rv[4 * ch + 3] = v4.w;
+          }
+          if constexpr (D == 64) {
+            tmem_st32(t_lane + C::kColK, rk);
+            tmem_st32(t_lane + C::kColV, rv);
+          } else {
+            tmem_st16(t_lane + C::kColK, rk);
+            tmem_st16(t_lane + C::kColV, rv);
+          }
+          tmem_st_wait();
+          tc_fence_before();
+          mbar_arrive(kv_tmem);
+        }
+      }
       for (int t = 0; t < n_q; ++t, ++T) {
         const int U = 2 * T + hh, s = U % kSl;
         mbar_wait(&slot_full[s], (U / kSl) & 1);  // (lse, Delta) of this half landed
