@@ -57,6 +57,7 @@ def _load():
             lib.oracle_attn_fwd_rows.argtypes = [d, ctypes.POINTER(i64), i64, d, d,
                                                  i64, i64, i64, i64, d, d]
             lib.oracle_attn_bwd.argtypes = [d, d, d, d, i64, i64, i64, i64, d, d, d, d, d, d]
+            lib.oracle_attn_bwd_dq_rows.argtypes = [d, d, ctypes.POINTER(i64), i64, d, d, i64, i64, i64, i64, d]
             lib.oracle_num_threads.restype = ctypes.c_int
             _lib = lib
     return _lib
@@ -104,6 +105,20 @@ def attn_fwd_rows(qrows, bh, k, v):
     _load().oracle_attn_fwd_rows(_ptr(qrows), bh.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), R,
                                  _ptr(k), _ptr(v), B, Nk, H, D, _ptr(out), _ptr(lse))
     return out, lse
+
+
+def attn_bwd_dq_rows(qrows, dorows, bh, k, v):
+    """Exact dQ for R explicit query rows (qrows, dorows [R][D]; bh [R][2]) of
+    self-attention over k, v [B][N][H][D].  Returns dq_rows [R][D]."""
+    qrows, dorows, k, v = _f64(qrows), _f64(dorows), _f64(k), _f64(v)
+    bh = np.ascontiguousarray(np.asarray(bh, dtype=np.int64))
+    R, D = qrows.shape
+    B, Nk, H, D2 = k.shape
+    assert D == D2 and dorows.shape == (R, D) and bh.shape == (R, 2)
+    out = np.empty((R, D), dtype=np.float64)
+    _load().oracle_attn_bwd_dq_rows(_ptr(qrows), _ptr(dorows), bh.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), R,
+                                    _ptr(k), _ptr(v), B, Nk, H, D, _ptr(out))
+    return out
 
 
 def attn_bwd(q, k, v, dout, with_abs: bool = False):

@@ -246,3 +246,41 @@ void oracle_attn_bwd(const double* q, const double* k, const double* v,
   free(delta);
   free(edelta);
 }
+
+/* dQ for an explicit list of R query rows (exact, per row):
+ *   P_ij = exp(s_ij - lse_i), Delta_i = dO_i . o_i with o_i, lse_i from the
+ *   row's own forward, dQ_i = scale sum_j P_ij (dO_i . v_j - Delta_i) k_j.
+ * qrows, dorows [R][D]; bh [R][2] = (batch, head) into k, v [B][Nk][H][D].
+ * Writes dq_rows [R][D].  Used for sampled backward checks at large N. */
+void oracle_attn_bwd_dq_rows(const double* qrows, const double* dorows, const int64_t* bh, int64_t R,
+                             const double* k, const double* v, int64_t B, int64_t Nk, int64_t H, int64_t D,
+                             double* dq_rows) {
+  (void)B;
+  const double scale = 1.0 / sqrt((double)D);
+  const int64_t rs = H * D;
+#pragma omp parallel
+  {
+    double* s = (double*)malloc(sizeof(double) * (size_t)(Nk > 0 ? Nk : 1));
+    double* o = (double*)malloc(sizeof(double) * (size_t)D);
+#pragma omp for schedule(dynamic, 1)
+    for (int64_t r = 0; r < R; ++r) {
+      const int64_t b = bh[2 * r], h = bh[2 * r + 1];
+      const double* kb = k + (b * Nk * H + h) * D;
+      const double* vb = v + (b * Nk * H + h) * D;
+      const double* qi = qrows + r * D;
+      const double* doi = dorows + r * D;
+      const double lse = attend_row(qi, kb, vb, Nk, rs, D, scale, s, o, NULL);
+      const double delta = dot(doi, o, D);
+      double* dqi = dq_rows + r * D;
+      for (int64_t d = 0; d < D; ++d) dqi[d] = 0.0;
+      for (int64_t j = 0; j < Nk; ++j) {
+        const double p = exp(s[j] - lse);
+        const double ds = p * (dot(doi, vb + j * rs, D) - delta);
+        for (int64_t d = 0; d < D; ++d) dqi[d] += ds * kb[j * rs + d];
+      }
+      for (int64_t d = 0; d < D; ++d) dqi[d] *= scale;
+    }
+    free(s);
+    free(o);
+  }
+}

@@ -7,12 +7,16 @@ computed by the CUDA path.
 
 Recipe (DESIGN.md "Input recipe"):
   * Q, K, V, dO ~ N(0, sigma^2) i.i.d. (sigma = 1 for the performance runs and
-    gate A; sigma_qk = 2 for Q and K in the sharpness gate B), drawn as float32
-    with numpy's PCG64 generator keyed by (seed, tensor id), then rounded to
-    bf16 (round-to-nearest-even, torch's conversion).
-  * The whole GLOBAL tensor [B][N][H][D] is drawn in one order and sequence
-    shards are slices of it, so the data are identical for every P.
-  * Seeds: q=1234, k=1235, v=1236, dO=1237 (offset by the test's seed).
+    gate A; sigma_qk = 2 for Q and K in the sharpness gate B), drawn as
+    float32 and rounded to bf16 (round-to-nearest-even, torch's conversion).
+  * Counter-based by construction: the values of tokens [1024 k, 1024 k + 1024)
+    of (tensor, batch b, head h) come from their own numpy PCG64 stream keyed
+    by (seed, tensor id, b, h, k).  Any rank can draw exactly its sequence
+    shard, and the oracle can redraw any head, without materialising the
+    global tensor (c5 is 4.3e9 values per tensor); the data are identical for
+    every P.
+  * Seeds: BASE_SEED = 1234 (offset by the test's seed); tensor ids q=0, k=1,
+    v=2, dO=3.
   * Shapes follow BASELINE.json configs (c1..c5); the paper's 188,416-token
     workload is 92 channels x 2,048 patches.
 """
@@ -23,6 +27,7 @@ import torch
 
 TENSOR_IDS = {"q": 0, "k": 1, "v": 2, "do": 3}
 BASE_SEED = 1234
+BLOCK = 1024
 
 # BASELINE.json "configs"; c3 and c4 list several P values, c5 is P=8.
 CONFIGS = {
@@ -34,28 +39,53 @@ CONFIGS = {
 }
 
 
-def normal_f32(shape, seed: int, name: str, sigma: float = 1.0) -> np.ndarray:
-    """float32 N(0, sigma^2) draws for tensor ``name`` (q/k/v/do)."""
-    rng = np.random.Generator(np.random.PCG64([int(seed), TENSOR_IDS[name]]))
-    x = rng.standard_normal(size=int(np.prod(shape)), dtype=np.float32).reshape(shape)
+def _block(seed: int, name: str, b: int, h: int, k: int, D: int) -> np.ndarray:
+    rng = np.random.Generator(np.random.PCG64([int(seed), TENSOR_IDS[name], int(b), int(h), int(k)]))
+    return rng.standard_normal(size=(BLOCK, D), dtype=np.float32)
+
+
+def normal_f32(B, N, H, D, seed: int, name: str, sigma: float = 1.0, n0: int = 0, n1: int | None = None,
+               heads=None) -> np.ndarray:
+    """float32 draws of tokens [n0, n1) and the listed heads (default all) of
+    the global [B][N][H][D] tensor ``name``: shape [B][n1-n0][len(heads)][D]."""
+    n1 = N if n1 is None else n1
+    heads = list(range(H)) if heads is None else list(heads)
+    out = np.empty((B, n1 - n0, len(heads), D), dtype=np.float32)
+
+    def fill(job):
+        b, hi, h = job
+        for k in range(n0 // BLOCK, (n1 + BLOCK - 1) // BLOCK):
+            lo, hi_ = max(n0, k * BLOCK), min(n1, (k + 1) * BLOCK)
+            out[b, lo - n0:hi_ - n0, hi, :] = _block(seed, name, b, h, k, D)[lo - k * BLOCK:hi_ - k * BLOCK]
+
+    jobs = [(b, hi, h) for b in range(B) for hi, h in enumerate(heads)]
+    if len(jobs) > 1 and (n1 - n0) * D >= (1 << 20):
+        from concurrent.futures import ThreadPoolExecutor  # numpy's generator releases the GIL
+        with ThreadPoolExecutor(max_workers=min(16, len(jobs))) as ex:
+            list(ex.map(fill, jobs))
+    else:
+        for job in jobs:
+            fill(job)
     if sigma != 1.0:
-        x *= np.float32(sigma)
-    return x
+        out *= np.float32(sigma)
+    return out
 
 
-def normal_bf16(shape, seed: int, name: str, sigma: float = 1.0) -> torch.Tensor:
+def normal_bf16(B, N, H, D, seed: int, name: str, sigma: float = 1.0, **kw) -> torch.Tensor:
     """bf16-rounded CPU tensor of the draws above."""
-    return torch.from_numpy(normal_f32(shape, seed, name, sigma)).to(torch.bfloat16)
+    return torch.from_numpy(normal_f32(B, N, H, D, seed, name, sigma, **kw)).to(torch.bfloat16)
 
 
-def qkv(B, N, H, D, seed: int = BASE_SEED, sigma_qk: float = 1.0, with_do: bool = False):
-    """Global bf16 CPU tensors (q, k, v[, dout]) of shape [B][N][H][D]."""
-    shape = (B, N, H, D)
-    out = [normal_bf16(shape, seed, "q", sigma_qk),
-           normal_bf16(shape, seed, "k", sigma_qk),
-           normal_bf16(shape, seed, "v")]
+def qkv(B, N, H, D, seed: int = BASE_SEED, sigma_qk: float = 1.0, with_do: bool = False, n0: int = 0,
+        n1: int | None = None, heads=None):
+    """bf16 CPU tensors (q, k, v[, dout]) of tokens [n0, n1) (default: the
+    whole sequence) and the listed heads of the global [B][N][H][D] tensors."""
+    kw = dict(n0=n0, n1=n1, heads=heads)
+    out = [normal_bf16(B, N, H, D, seed, "q", sigma_qk, **kw),
+           normal_bf16(B, N, H, D, seed, "k", sigma_qk, **kw),
+           normal_bf16(B, N, H, D, seed, "v", **kw)]
     if with_do:
-        out.append(normal_bf16(shape, seed, "do"))
+        out.append(normal_bf16(B, N, H, D, seed, "do", **kw))
     return tuple(out)
 
 

@@ -1,0 +1,109 @@
+"""Multi-rank check at the BASELINE configs' full sizes (c3, c4, c5), launched
+by tests/test_multigpu.py as
+    torchrun --nproc-per-node P tests/mp_bigconfig_check.py --config c4
+Each rank draws exactly its sequence shard from synth (counter-based), runs the
+Ulysses forward + backward through the C ABI in the bench's configuration, and
+checks against the fp64 oracle what the oracle can compute row by row:
+  * out / lse at sampled query rows (first / last token of every rank's shard,
+    both sides of every shard boundary, random rows) for two heads that live on
+    different ranks after the all-to-all (head 0 and head H-1);
+  * dQ at the same sampled rows (oracle.attn_bwd_dq_rows, exact per row);
+  * dK / dV through invariants that hold at any size, per head, reduced over
+    ranks: sum_j dK_j = 0, sum_j dV_j = sum_i dO_i, <Q, dQ> = <K, dK>;
+  * everything finite; a2a call law (2 + 2).
+Prints "BIG_OK" on rank 0 on success."""
+import argparse
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import oracle  # noqa: E402
+import paper_2405_15780_b200 as ua  # noqa: E402
+import synth  # noqa: E402
+from tests.parity import gate_grad, gate_lse, gate_out  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="c4")
+    ap.add_argument("--rows", type=int, default=4, help="random rows per rank (plus boundary rows)")
+    a = ap.parse_args()
+    cfg = synth.CONFIGS[a.config]
+    B, N, H, D = cfg["B"], cfg["N"], cfg["H"], cfg["D"]
+    rank, P = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    Nl = N // P
+    seed = synth.BASE_SEED
+    q, k, v, do = synth.qkv(B, N, H, D, seed=seed, with_do=True, n0=rank * Nl, n1=(rank + 1) * Nl)
+    qs, ks, vs, ds = (t.to(dev) for t in (q, k, v, do))
+
+    ctx = ua.Context(P=P, rank=rank, device=local)
+    c0, _ = ctx.comm_stats()
+    r = ua.ulysses_attn_fwd(ctx, qs, ks, vs)
+    dq, dk, dv = ua.ulysses_attn_bwd(ctx, qs, ks, vs, r.out, r.lse, ds)
+    torch.cuda.synchronize()
+    c1, _ = ctx.comm_stats()
+    assert c1 - c0 == (4 if P > 1 else 0)
+    for t in (r.out, r.lse, dq, dk, dv):
+        assert torch.isfinite(t.float()).all()
+
+    # ---- sampled rows of this rank's shard, heads 0 and H-1
+    heads = [0, H - 1]
+    rng = np.random.default_rng(100 + rank)
+    rows = sorted(set([0, 1, Nl - 1, Nl - 2] + list(rng.integers(0, Nl, a.rows))))
+    kf = synth.to_f64(synth.normal_bf16(B, N, H, D, seed, "k", heads=heads))
+    vf = synth.to_f64(synth.normal_bf16(B, N, H, D, seed, "v", heads=heads))
+    bh = np.array([(0, hi) for hi in range(len(heads)) for _ in rows])
+    idx = np.array(rows * len(heads))
+    hsel = np.array([heads[x] for x in bh[:, 1]])
+    ti, th = torch.from_numpy(idx), torch.from_numpy(hsel)
+    qrows = synth.to_f64(q[0, ti, th])
+    dorows = synth.to_f64(do[0, ti, th])
+    o_ref, l_ref = oracle.attn_fwd_rows(qrows, bh, kf, vf)
+    dq_ref = oracle.attn_bwd_dq_rows(qrows, dorows, bh, kf, vf)
+    out_np = r.out[0, ti.to(dev), th.to(dev)].float().cpu().numpy()
+    dq_np = dq[0, ti.to(dev), th.to(dev)].float().cpu().numpy()
+    gate_out(out_np, o_ref)
+    gate_grad(dq_np, dq_ref)
+    # lse: rank j holds heads [j*H/P, (j+1)*H/P) for all tokens
+    hl = H // P
+    lse_np = r.lse.cpu().numpy()
+    for hi, h in enumerate(heads):
+        if rank * hl <= h < (rank + 1) * hl:
+            # lse of this rank's sampled rows is also checked on the head owner (global token index)
+            gi = np.array(rows) + rank * Nl
+            sel = bh[:, 1] == hi
+            gate_lse(lse_np[0, h - rank * hl, gi], l_ref[sel])
+
+    # ---- dK / dV invariants, per head, summed over ranks
+    qd, kd, dod = (x.to(torch.float64) for x in (qs, ks, ds))
+    s = torch.stack([
+        dk.double().sum(dim=(0, 1)),                                  # [H][D]
+        dv.double().sum(dim=(0, 1)) - dod.sum(dim=(0, 1)),
+    ])
+    inner = torch.stack([(qd * dq.double()).sum(dim=(0, 1, 3)), (kd * dk.double()).sum(dim=(0, 1, 3))])
+    mags = torch.stack([dk.double().abs().sum(dim=(0, 1)), dv.double().abs().sum(dim=(0, 1))])
+    imag = torch.stack([(qd * dq.double()).abs().sum(dim=(0, 1, 3)), (kd * dk.double()).abs().sum(dim=(0, 1, 3))])
+    for t in (s, inner, mags, imag):
+        dist.all_reduce(t)
+    if rank == 0:
+        assert (s[0].abs() <= 1e-2 * mags[0] + 1e-3).all(), "sum_j dK_j != 0"
+        assert (s[1].abs() <= 1e-2 * mags[1] + 1e-3).all(), "sum_j dV_j != sum_i dO_i"
+        assert ((inner[0] - inner[1]).abs() <= 1e-2 * (imag[0] + imag[1]) + 1e-3).all(), "<Q,dQ> != <K,dK>"
+        print("BIG_OK", a.config, "P", P, flush=True)
+    ctx.close()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

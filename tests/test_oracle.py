@@ -320,3 +320,13 @@ def test_bwd_abs_helpers():
         E = P * np.abs(do[0, :, h] * O).sum(1, keepdims=True)
         assert np.abs(aq[0, :, h] - sc * (np.abs(dS) + E) @ np.abs(k[0, :, h])).max() < 1e-12
         assert np.abs(ak[0, :, h] - sc * (np.abs(dS) + E).T @ np.abs(q[0, :, h])).max() < 1e-12
+
+
+def test_bwd_dq_rows_matches_dense():
+    B, N, H, D = 2, 70, 3, 16
+    q, k, v, do = (rnd((B, N, H, D), s) for s in (110, 111, 112, 113))
+    dq, _, _, _, _ = oracle.attn_bwd(q, k, v, do)
+    bh = np.array([[0, 0], [1, 2], [1, 1], [0, 2]])
+    idx = np.array([0, 69, 33, 5])
+    got = oracle.attn_bwd_dq_rows(q[bh[:, 0], idx, bh[:, 1]], do[bh[:, 0], idx, bh[:, 1]], bh, k, v)
+    assert np.abs(got - dq[bh[:, 0], idx, bh[:, 1]]).max() < 1e-13
