@@ -26,6 +26,7 @@
 //    because O and l carry the same stale max.
 #include "attn_common.cuh"
 #include "attn_kernels.h"
+#include "trace.cuh"
 
 // Tuning knobs (defaults are the shipped configuration; scripts/ab.py builds
 // variants with -D overrides).
@@ -121,7 +122,9 @@ __global__ void __launch_bounds__(384, 1) attn_fwd_kernel(const __grid_constant_
                       q0 + t * 128, h, b, kEvictFirst);
       for (int j = 0; j < n_kv; ++j) {
         const int s = j % kStages;
+        UA_TEV(0, j, 1);
         if (j >= kStages) mbar_wait(&kv_empty[s], ((j / kStages) & 1) ^ 1);
+        UA_TEV(0, j, 2);
         const int row = (kv_t0 + j) * 128;
         mbar_arrive_expect_tx(&k_full[s], G::kTileBytes);
         for (int a = 0; a < G::kAtoms; ++a)
@@ -185,13 +188,17 @@ __global__ void __launch_bounds__(384, 1) attn_fwd_kernel(const __grid_constant_
       for (int j = 0; j <= n_kv; ++j) {
         const int s = j % kStages;
         if (j < n_kv) {
+          UA_TEV(1, j, 1);
           mbar_wait(&k_full[s], (j / kStages) & 1);
+          UA_TEV(1, j, 2);
           tc_fence_after();
         }
         for (int t = 0; t < 2; ++t) {
           if (j > 0) {  // O_t += P_t(j-1) V_{j-1}
             const int sp = (j - 1) % kStages;
+            UA_TEV(1, j, 10 + t);
             mbar_wait(&p_full[t], (j - 1) & 1);
+            UA_TEV(1, j, 12 + t);
             if (t == 0) mbar_wait(&v_full[sp], ((j - 1) / kStages) & 1);
             tc_fence_after();
             const uint32_t vt = sVa + sp * G::kTileBytes;
@@ -208,6 +215,7 @@ __global__ void __launch_bounds__(384, 1) attn_fwd_kernel(const __grid_constant_
               mma_ss(tbase + C::kColS + t * 128, kmajor_desc<D>(qt, kk), kmajor_desc<D>(kt, kk), idesc_s,
                      kk > 0 ? 1u : 0u);
             mma_commit(&s_full[t]);
+            UA_TEV(1, j, 14 + t);
           }
         }
         if (j > 0) mma_commit(&kv_empty[(j - 1) % kStages]);
@@ -227,7 +235,9 @@ __global__ void __launch_bounds__(384, 1) attn_fwd_kernel(const __grid_constant_
     float m_use = -INFINITY, l = 0.f;
 
     for (int j = 0; j < n_kv; ++j) {
+      if (row == 0) UA_TEV(2 + t, j, 1);
       mbar_wait(&s_full[t], j & 1);
+      if (row == 0) UA_TEV(2 + t, j, 2);
       tc_fence_after();
       float sv[128];
 #pragma unroll
@@ -257,6 +267,7 @@ __global__ void __launch_bounds__(384, 1) attn_fwd_kernel(const __grid_constant_
       }
       const float rmax = fmax3(mx[0], mx[1], fmaxf(mx[2], mx[3]));
       const float m_new = fmaxf(m_use, rmax * c);
+      if (row == 0) UA_TEV(2 + t, j, 4);
       const bool need = m_new > m_use + C::kRescaleThreshold;
       const bool warp_need = __any_sync(0xffffffffu, need);
       const float alpha = need ? ex2(m_use - m_new) : 1.f;
@@ -301,9 +312,11 @@ __global__ void __launch_bounds__(384, 1) attn_fwd_kernel(const __grid_constant_
           tmem_st32(t_lane + colO + cc, r);
         }
       }
+      if (row == 0) UA_TEV(2 + t, j, 5);
       tmem_st_wait();
       tc_fence_before();
       mbar_arrive(&p_full[t]);
+      if (row == 0) UA_TEV(2 + t, j, 6);
     }
 
     // ------------------------------------------------------------ epilogue
@@ -356,7 +369,13 @@ cudaError_t launch_fwd_impl(const FwdParams& p, int B, int Hx, cudaStream_t stre
     attr_set = true;
   }
   dim3 grid((p.n_q + 255) / 256, Hx, B);
+#if UA_TRACE
+  trace_reset();
+#endif
   attn_fwd_kernel<D><<<grid, C::kThreads, C::kSmemBytes, stream>>>(p);
+#if UA_TRACE
+  trace_dump("fwd");
+#endif
   return cudaGetLastError();
 }
 
