@@ -36,6 +36,9 @@
 #ifndef UA_FWD_POLY_MOD
 #define UA_FWD_POLY_MOD 3   // every UA_FWD_POLY_MOD-th exp2 pair on the FMA pipe (0: none)
 #endif
+#ifndef UA_FWD_PINGPONG
+#define UA_FWD_PINGPONG 1   // the two softmax warpgroups take turns for their exp2 phases
+#endif
 
 namespace ua {
 
@@ -233,6 +236,12 @@ __global__ void __launch_bounds__(384, 1) attn_fwd_kernel(const __grid_constant_
     const uint32_t colP = C::kColP + t * C::kPStride;
     const float c = p.scale_log2;
     float m_use = -INFINITY, l = 0.f;
+    // Exp-phase ping-pong: warpgroup t runs its exp2 / P-store phase only after
+    // the other warpgroup finished its own (named barriers 1 and 2, 256
+    // threads), so the two tiles' exponentials do not share the MUFU unit and
+    // one tile's GEMMs run under the other tile's exponentials.
+    const uint32_t bar_mine = 1 + t, bar_other = 2 - t;
+    if (UA_FWD_PINGPONG && t == 1) named_bar_arrive(1, 256);  // tile 0 goes first
 
     for (int j = 0; j < n_kv; ++j) {
       if (row == 0) UA_TEV(2 + t, j, 1);
@@ -277,6 +286,7 @@ __global__ void __launch_bounds__(384, 1) attn_fwd_kernel(const __grid_constant_
       }
       // p = 2^(s*c - m): packed fp32x2 FFMA for the argument, MUFU ex2 or the
       // FMA-pipe polynomial for the power, packed FADD for the row sum.
+      if (UA_FWD_PINGPONG) named_bar_sync(bar_mine, 256);
       const float2 c2 = make_float2(c, c), nm2 = make_float2(-m_use, -m_use);
       float2 ls[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
       if (C::kSeparateP && j > 0) {  // P_t buffer free: PV_t(j-1) has consumed it
@@ -298,6 +308,7 @@ __global__ void __launch_bounds__(384, 1) attn_fwd_kernel(const __grid_constant_
         tmem_st16(t_lane + colP + cc / 2, pk);
       }
       l += (ls[0].x + ls[0].y) + (ls[1].x + ls[1].y);
+      if (UA_FWD_PINGPONG) named_bar_arrive(bar_other, 256);
       // Lazy rescale of O_t, after PV_t(j-1) has completed (o_done).
       if (warp_need && j > 0) {
         mbar_wait(&o_done[t], (j - 1) & 1);
@@ -318,6 +329,8 @@ __global__ void __launch_bounds__(384, 1) attn_fwd_kernel(const __grid_constant_
       mbar_arrive(&p_full[t]);
       if (row == 0) UA_TEV(2 + t, j, 6);
     }
+
+    if (UA_FWD_PINGPONG && t == 0) named_bar_sync(1, 256);  // consume tile 1's last hand-back
 
     // ------------------------------------------------------------ epilogue
     mbar_wait(&o_done[t], (n_kv - 1) & 1);

@@ -1,8 +1,9 @@
 // trace.cuh — optional per-event clock64 tracing of one CTA (tuning aid).
 // Compiled in only with -DUA_TRACE=1 (a variant build, see build.py); the
-// shipped library contains none of it.  Records (clock64, role, tile, event)
-// for the CTA with blockIdx.x == UA_TRACE_CTA into a device buffer that the
-// host dumps to $UA_TRACE_FILE after the launch.
+// shipped library contains none of it.  Each (role, tile, event) of the CTA
+// with blockIdx == (UA_TRACE_CTA, 0, 0) stores clock64() into its own slot of
+// a device buffer (plain stores, no atomics, so the timeline is not
+// perturbed); the host dumps the non-zero slots to $UA_TRACE_FILE.
 #pragma once
 #include <cstdint>
 
@@ -16,35 +17,30 @@
 #if UA_TRACE
 #include <cstdio>
 #include <cstdlib>
+#include <vector>
 namespace ua {
-constexpr int kTraceCap = 1 << 16;
-__device__ unsigned long long g_trace[kTraceCap * 2];
-__device__ unsigned int g_trace_n;
+constexpr int kTraceRoles = 8, kTraceTiles = 4096, kTraceEvents = 32;
+constexpr int kTraceSlots = kTraceRoles * kTraceTiles * kTraceEvents;
+__device__ unsigned long long g_trace[kTraceSlots];
 __device__ __forceinline__ void trace_ev(int role, int tile, int ev) {
-  if (blockIdx.x != UA_TRACE_CTA || blockIdx.y != 0 || blockIdx.z != 0) return;
-  unsigned int i = atomicAdd(&g_trace_n, 1u);
-  if (i < kTraceCap) {
-    g_trace[2 * i] = clock64();
-    g_trace[2 * i + 1] = (unsigned long long)((role << 24) | (tile << 8) | ev);
-  }
+  if (blockIdx.x != UA_TRACE_CTA || blockIdx.y != 0 || blockIdx.z != 0 || tile >= kTraceTiles) return;
+  g_trace[(role * kTraceTiles + tile) * kTraceEvents + ev] = clock64();
 }
 inline void trace_reset() {
-  unsigned int z = 0;
-  cudaMemcpyToSymbol(g_trace_n, &z, sizeof(z));
+  static std::vector<unsigned long long> z(kTraceSlots, 0ull);
+  cudaMemcpyToSymbol(g_trace, z.data(), sizeof(unsigned long long) * kTraceSlots);
 }
 inline void trace_dump(const char* tag) {
   cudaDeviceSynchronize();
-  unsigned int n = 0;
-  cudaMemcpyFromSymbol(&n, g_trace_n, sizeof(n));
-  if (n > kTraceCap) n = kTraceCap;
-  static unsigned long long buf[kTraceCap * 2];
-  cudaMemcpyFromSymbol(buf, g_trace, sizeof(unsigned long long) * 2 * n);
+  static std::vector<unsigned long long> buf(kTraceSlots);
+  cudaMemcpyFromSymbol(buf.data(), g_trace, sizeof(unsigned long long) * kTraceSlots);
   const char* path = std::getenv("UA_TRACE_FILE");
   FILE* f = std::fopen(path ? path : "ua_trace.txt", "a");
   if (!f) return;
-  for (unsigned int i = 0; i < n; ++i)
-    std::fprintf(f, "%s %llu %llu %llu %llu\n", tag, buf[2 * i], buf[2 * i + 1] >> 24, (buf[2 * i + 1] >> 8) & 0xFFFF,
-                 buf[2 * i + 1] & 0xFF);
+  for (int i = 0; i < kTraceSlots; ++i)
+    if (buf[i])
+      std::fprintf(f, "%s %llu %d %d %d\n", tag, buf[i], i / (kTraceTiles * kTraceEvents),
+                   (i / kTraceEvents) % kTraceTiles, i % kTraceEvents);
   std::fclose(f);
 }
 }  // namespace ua
