@@ -37,7 +37,10 @@
 #define UA_FWD_POLY_MOD 3   // every UA_FWD_POLY_MOD-th exp2 pair on the FMA pipe (0: none)
 #endif
 #ifndef UA_FWD_PINGPONG
-#define UA_FWD_PINGPONG 1   // the two softmax warpgroups take turns for their exp2 phases
+#define UA_FWD_PINGPONG 0   // the two softmax warpgroups take turns for their exp2 phases (A/B: slower)
+#endif
+#ifndef UA_FWD_RELOAD
+#define UA_FWD_RELOAD 1     // two TMEM passes over S (max, then exp) instead of holding 128 values
 #endif
 
 namespace ua {
@@ -248,6 +251,31 @@ __global__ void __launch_bounds__(384, 1) attn_fwd_kernel(const __grid_constant_
       mbar_wait(&s_full[t], j & 1);
       if (row == 0) UA_TEV(2 + t, j, 2);
       tc_fence_after();
+      const int kv0 = p.kv_begin + j * 128;
+      const bool tail = kv0 + 128 > p.kv_end;
+#if UA_FWD_RELOAD
+      // Two passes over S in TMEM (row max, then exponentials) so only one or
+      // two 32-column chunks are live in registers: the register file then has
+      // room for many independent exp2 chains in flight.
+      float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+      for (int cc = 0; cc < 128; cc += 32) {
+        uint32_t r[32];
+        tmem_ld32(t_lane + colS + cc, r);
+        tmem_ld_wait();
+        if (tail) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (kv0 + cc + i >= p.kv_end) r[i] = __float_as_uint(-INFINITY);
+        }
+#pragma unroll
+        for (int i = 0; i < 32; i += 8) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            mx[u] = fmax3(mx[u], __uint_as_float(r[i + 2 * u]), __uint_as_float(r[i + 2 * u + 1]));
+        }
+      }
+#else
       float sv[128];
 #pragma unroll
       for (int cc = 0; cc < 128; cc += 32) {
@@ -261,8 +289,7 @@ __global__ void __launch_bounds__(384, 1) attn_fwd_kernel(const __grid_constant_
         tc_fence_before();
         mbar_arrive(&s_free[t]);
       }
-      const int kv0 = p.kv_begin + j * 128;
-      if (kv0 + 128 > p.kv_end) {
+      if (tail) {
 #pragma unroll
         for (int i = 0; i < 128; ++i)
           if (kv0 + i >= p.kv_end) sv[i] = -INFINITY;
@@ -274,6 +301,7 @@ __global__ void __launch_bounds__(384, 1) attn_fwd_kernel(const __grid_constant_
 #pragma unroll
         for (int u = 0; u < 4; ++u) mx[u] = fmax3(mx[u], sv[i + 2 * u], sv[i + 2 * u + 1]);
       }
+#endif
       const float rmax = fmax3(mx[0], mx[1], fmaxf(mx[2], mx[3]));
       const float m_new = fmaxf(m_use, rmax * c);
       if (row == 0) UA_TEV(2 + t, j, 4);
@@ -293,6 +321,38 @@ __global__ void __launch_bounds__(384, 1) attn_fwd_kernel(const __grid_constant_
         mbar_wait(&o_done[t], (j - 1) & 1);
         tc_fence_after();
       }
+#if UA_FWD_RELOAD
+      // software-pipelined: chunk k+1 is loaded from TMEM while chunk k is exponentiated
+      uint32_t ra[32], rb[32];
+      tmem_ld32(t_lane + colS, ra);
+      tmem_ld_wait();
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        uint32_t* cur = (k & 1) ? rb : ra;
+        uint32_t* nxt = (k & 1) ? ra : rb;
+        if (k < 3) tmem_ld32(t_lane + colS + 32 * (k + 1), nxt);
+        if (tail) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (kv0 + 32 * k + i >= p.kv_end) cur[i] = __float_as_uint(-INFINITY);
+        }
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const float2 x = __ffma2_rn(make_float2(__uint_as_float(cur[2 * i]), __uint_as_float(cur[2 * i + 1])), c2, nm2);
+          const bool poly = C::kPolyExp && UA_FWD_POLY_MOD > 0 && (i % (UA_FWD_POLY_MOD > 0 ? UA_FWD_POLY_MOD : 1)) == 1;
+          const float2 pp = poly ? exp2_poly2(x) : make_float2(ex2(x.x), ex2(x.y));
+          ls[i & 1] = __fadd2_rn(ls[i & 1], pp);
+          pk[i] = pack_bf16x2(pp.x, pp.y);
+        }
+        tmem_st16(t_lane + colP + 16 * k, pk);
+        if (k < 3) tmem_ld_wait();
+      }
+      if constexpr (C::kSeparateP) {  // S_t fully consumed: the next Q K^T may overwrite it
+        tc_fence_before();
+        mbar_arrive(&s_free[t]);
+      }
+#else
 #pragma unroll
       for (int cc = 0; cc < 128; cc += 32) {
         uint32_t pk[16];
@@ -307,6 +367,7 @@ __global__ void __launch_bounds__(384, 1) attn_fwd_kernel(const __grid_constant_
         }
         tmem_st16(t_lane + colP + cc / 2, pk);
       }
+#endif
       l += (ls[0].x + ls[0].y) + (ls[1].x + ls[1].y);
       if (UA_FWD_PINGPONG) named_bar_arrive(bar_other, 256);
       // Lazy rescale of O_t, after PV_t(j-1) has completed (o_done).
