@@ -40,7 +40,7 @@
 #define UA_FWD_PINGPONG 0   // the two softmax warpgroups take turns for their exp2 phases (A/B: slower)
 #endif
 #ifndef UA_FWD_RELOAD
-#define UA_FWD_RELOAD 1     // two TMEM passes over S (max, then exp) instead of holding 128 values
+#define UA_FWD_RELOAD 0     // two TMEM passes over S (max, then exp); A/B: slower, kept as an option
 #endif
 
 namespace ua {
