@@ -177,6 +177,8 @@ def main():
     ap.add_argument("--H", type=int, default=WORKLOAD["H"])
     ap.add_argument("--D", type=int, default=WORKLOAD["D"])
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--a2a", default="nccl", choices=["nccl", "peer"],
+                    help="all-to-all transport for P > 1: NCCL send/recv, or NVLink peer stores from the kernels")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
@@ -198,6 +200,8 @@ def main():
     ua.validate(B, N, H, D, P)
     Nl = N // P
     ctx = ua.Context(P=P, rank=rank, device=local)
+    if P > 1:
+        ctx.set_a2a_mode(args.a2a)
     dev = torch.device("cuda", local)
     g = torch.Generator(device=dev).manual_seed(1234 + rank)
     shape = (B, Nl, H, D)
@@ -325,7 +329,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": f"c4: Ulysses attention fwd+bwd, N={N} tokens, H={H}, D={D}, B={B}, P={P}",
-                       "B": B, "N": N, "H": H, "D": D, "P": P, "parallelism": f"ulysses-sp{P}",
+                       "B": B, "N": N, "H": H, "D": D, "P": P, "parallelism": f"ulysses-sp{P}", "a2a": args.a2a if P > 1 else "none",
                        "l2": "inputs larger than L2 (each q/k/v/dO shard "
                              f"{q.numel() * 2 / 1e6:.0f} MB; working set > 126 MB)",
                        "inputs": "N(0,1) bf16, torch.randn seeded per rank"},

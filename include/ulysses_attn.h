@@ -109,6 +109,22 @@ enum {
   UA_NUM_PHASES
 };
 ua_status ua_ctx_enable_timing(ua_ctx* ctx, int enable);
+
+/* How the all-to-alls move data when P > 1:
+ *  UA_A2A_NCCL  pack -> ncclSend/ncclRecv group -> unpack (default).
+ *  UA_A2A_PEER  no NCCL on the data path: the pack kernel stores every head
+ *               chunk straight into the owning GPU's receive buffer over
+ *               NVLink, and the attention epilogues (O forward; dK, dV and the
+ *               dQ finaliser backward) store each row straight into the token
+ *               owner's buffer; completion is a system-scope flag per peer.
+ *               The receive buffers are library-owned device memory, CUDA-IPC
+ *               mapped on every rank (allocated on first use per shape; the
+ *               handles travel over the ctx's NCCL communicator).
+ * Collective: every rank sets the same mode before its next call.
+ * UA_ERR_UNSUPPORTED if P == 1 or the peer mappings cannot be created. */
+enum { UA_A2A_NCCL = 0, UA_A2A_PEER = 1 };
+ua_status ua_ctx_set_a2a_mode(ua_ctx* ctx, int mode);
+ua_status ua_ctx_get_a2a_mode(const ua_ctx* ctx, int* mode);
 ua_status ua_ctx_phase_times(ua_ctx* ctx, double* ms, int64_t* launches);
 
 /* ------------------------------------------------------------- forward

@@ -28,7 +28,7 @@ STATUS = {0: "UA_OK", 1: "UA_ERR_INVALID_ARG", 2: "UA_ERR_HEAD_DIVISIBILITY", 3:
 # Every symbol include/ulysses_attn.h declares.
 EXPORTS = ("ua_version", "ua_status_string", "ua_last_error", "ua_validate", "ua_workspace_size",
            "ua_get_unique_id", "ua_ctx_create", "ua_ctx_destroy", "ua_ctx_comm_stats",
-           "ua_ctx_enable_timing", "ua_ctx_phase_times",
+           "ua_ctx_enable_timing", "ua_ctx_phase_times", "ua_ctx_set_a2a_mode", "ua_ctx_get_a2a_mode",
            "ua_ulysses_attn_fwd", "ua_ulysses_attn_bwd", "ua_attn_fwd_segment", "ua_lse_merge",
            "ua_f32_to_bf16_bnhd")
 
@@ -73,6 +73,8 @@ def lib():
         L.ua_ctx_destroy.argtypes = [vp]
         L.ua_ctx_comm_stats.argtypes = [vp, ctypes.POINTER(i64), ctypes.POINTER(i64)]
         L.ua_ctx_enable_timing.argtypes = [vp, i32]
+        L.ua_ctx_set_a2a_mode.argtypes = [vp, i32]
+        L.ua_ctx_get_a2a_mode.argtypes = [vp, ctypes.POINTER(i32)]
         L.ua_ctx_phase_times.argtypes = [vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i64)]
         L.ua_ulysses_attn_fwd.argtypes = [vp, vp, vp, vp, vp, vp, i64, i64, i32, i32, i32, vp, sz, vp]
         L.ua_ulysses_attn_bwd.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, i64, i64, i32, i32, i32, vp, sz, vp]
@@ -168,6 +170,18 @@ class Context:
         c, b = ctypes.c_int64(0), ctypes.c_int64(0)
         _check(lib().ua_ctx_comm_stats(self._h, ctypes.byref(c), ctypes.byref(b)))
         return c.value, b.value
+
+    A2A_MODES = {"nccl": 0, "peer": 1}
+
+    def set_a2a_mode(self, mode: str):
+        """'nccl' (pack -> NCCL send/recv -> unpack) or 'peer' (kernels store
+        straight into the owning GPU's buffers over NVLink).  Collective."""
+        _check(lib().ua_ctx_set_a2a_mode(self._h, self.A2A_MODES[mode]))
+
+    def a2a_mode(self) -> str:
+        m = ctypes.c_int(0)
+        _check(lib().ua_ctx_get_a2a_mode(self._h, ctypes.byref(m)))
+        return {v: k for k, v in self.A2A_MODES.items()}[m.value]
 
     def enable_timing(self, on: bool = True):
         _check(lib().ua_ctx_enable_timing(self._h, 1 if on else 0))

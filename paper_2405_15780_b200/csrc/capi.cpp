@@ -32,6 +32,16 @@ struct ua_ctx {
   };
   std::vector<Rec> pending;
   std::vector<cudaEvent_t> pool;
+  // NVLink peer-store all-to-all (UA_A2A_PEER): library-owned buffers, CUDA IPC
+  // mapped on every rank (peer[k] = rank k's copy, peer[rank] = local).
+  int a2a_mode = UA_A2A_NCCL;
+  struct PeerBuf {
+    void* local = nullptr;
+    size_t bytes = 0;
+    void* peer[ua::kMaxPeers] = {};
+  };
+  PeerBuf flags, fwd_in, fwd_out, bwd_in, bwd_out;
+  int64_t step_fwd = 0, step_bwd = 0;
   cudaEvent_t get_event() {
     if (!pool.empty()) {
       cudaEvent_t e = pool.back();
@@ -229,13 +239,14 @@ ua_status check_async(ua_ctx* ctx) {
 ua_status launch_attention_fwd(const void* q, const void* k, const void* v, int64_t sn, int64_t sh, int64_t sb,
                                ua::ViewArg o, float* o_f32, int64_t of_sn, int64_t of_sh, int64_t of_sb, float* lse,
                                int64_t l_sh, int64_t l_sb, int64_t B, int64_t N, int heads, int D, int64_t kv_begin,
-                               int64_t kv_end, cudaStream_t stream) {
+                               int64_t kv_end, cudaStream_t stream, const ua::PeerOut* o_peer = nullptr) {
   ua::FwdParams p;
   std::memset(&p, 0, sizeof(p));
   UA_TRY(make_map(&p.tm_q, q, D, N, heads, B, sn, sh, sb));
   UA_TRY(make_map(&p.tm_k, k, D, N, heads, B, sn, sh, sb));
   UA_TRY(make_map(&p.tm_v, v, D, N, heads, B, sn, sh, sb));
   p.o = o;
+  if (o_peer) p.o_peer = *o_peer;
   p.o_f32 = o_f32;
   p.of_sn = of_sn; p.of_sh = of_sh; p.of_sb = of_sb;
   p.lse = lse;
@@ -252,9 +263,12 @@ ua_status launch_attention_bwd(const void* q, const void* k, const void* v, cons
                                int64_t sb, ua::ViewArg dk, ua::ViewArg dv, float* dq_acc, const float* lse,
                                int64_t l_sh, int64_t l_sb, const float* delta, int64_t d_sn, int64_t d_sh,
                                int64_t d_sb, int64_t B, int64_t N, int heads, int D, float2* lsed,
-                               cudaStream_t stream) {
+                               cudaStream_t stream, const ua::PeerOut* dk_peer = nullptr,
+                               const ua::PeerOut* dv_peer = nullptr) {
   ua::BwdParams p;
   std::memset(&p, 0, sizeof(p));
+  if (dk_peer) p.dk_peer = *dk_peer;
+  if (dv_peer) p.dv_peer = *dv_peer;
   // (-lse*log2e, Delta) per query row, contiguous per head (bulk-loaded by the kernel)
   UA_CUDA(ua::launch_bwd_prep(lse, l_sh, l_sb, delta, d_sn, d_sh, d_sb, lsed, B, heads, N, stream));
   p.lsed = lsed;
@@ -282,6 +296,74 @@ ua_status launch_attention_bwd(const void* q, const void* k, const void* v, cons
   UA_CUDA(ua::launch_attn_bwd(p, D, int(B), heads, stream));
   return UA_OK;
 }
+
+// ------------------------------------------------------------ peer all-to-all
+// Collective: exchange CUDA IPC handles of `pb.local` through the ctx's NCCL
+// communicator and open every peer's copy (the buffers are library-owned, so
+// the mapping is done once per shape, not per call).
+ua_status peer_exchange(ua_ctx* ctx, ua_ctx::PeerBuf& pb, cudaStream_t stream) {
+  cudaIpcMemHandle_t mine;
+  UA_CUDA(cudaIpcGetMemHandle(&mine, pb.local));
+  const int P = ctx->P;
+  char* d = nullptr;
+  UA_CUDA(cudaMalloc(&d, sizeof(cudaIpcMemHandle_t) * (P + 1)));
+  UA_CUDA(cudaMemcpyAsync(d + sizeof(mine) * P, &mine, sizeof(mine), cudaMemcpyHostToDevice, stream));
+  UA_NCCL(ncclAllGather(d + sizeof(mine) * P, d, sizeof(mine), ncclUint8, ctx->comm, stream));
+  std::vector<cudaIpcMemHandle_t> all(P);
+  UA_CUDA(cudaMemcpyAsync(all.data(), d, sizeof(mine) * P, cudaMemcpyDeviceToHost, stream));
+  UA_CUDA(cudaStreamSynchronize(stream));
+  cudaFree(d);
+  for (int k = 0; k < P; ++k) {
+    if (k == ctx->rank) {
+      pb.peer[k] = pb.local;
+    } else {
+      UA_CUDA(cudaIpcOpenMemHandle(&pb.peer[k], all[k], cudaIpcMemLazyEnablePeerAccess));
+    }
+  }
+  return UA_OK;
+}
+
+void peer_release(ua_ctx* ctx, ua_ctx::PeerBuf& pb) {
+  for (int k = 0; k < ctx->P; ++k)
+    if (k != ctx->rank && pb.peer[k]) cudaIpcCloseMemHandle(pb.peer[k]);
+  if (pb.local) cudaFree(pb.local);
+  pb = ua_ctx::PeerBuf();
+}
+
+// Collective (all ranks call with the same shape): make sure `pb` holds at
+// least `bytes`, re-allocating and re-mapping when it grows.
+ua_status peer_ensure(ua_ctx* ctx, ua_ctx::PeerBuf& pb, size_t bytes, cudaStream_t stream) {
+  if (pb.local && pb.bytes >= bytes) return UA_OK;
+  // every rank has drained its previous steps before anyone unmaps / frees
+  UA_CUDA(cudaDeviceSynchronize());
+  int* dummy = nullptr;
+  UA_CUDA(cudaMalloc(&dummy, sizeof(int)));
+  UA_NCCL(ncclAllReduce(dummy, dummy, 1, ncclInt32, ncclSum, ctx->comm, stream));
+  UA_CUDA(cudaStreamSynchronize(stream));
+  cudaFree(dummy);
+  peer_release(ctx, pb);
+  UA_CUDA(cudaMalloc(&pb.local, bytes));
+  UA_CUDA(cudaMemset(pb.local, 0, bytes));
+  pb.bytes = bytes;
+  return peer_exchange(ctx, pb, stream);
+}
+
+ua::PeerFlags peer_flags(const ua_ctx* ctx) {
+  ua::PeerFlags f{};
+  for (int k = 0; k < ctx->P; ++k) f.peer[k] = static_cast<int64_t*>(ctx->flags.peer[k]);
+  return f;
+}
+
+ua::PeerOut peer_out(const ua_ctx::PeerBuf& pb, size_t offset, const Shape& s, int rank) {
+  ua::PeerOut o{};
+  for (int k = 0; k < s.P; ++k) o.base[k] = static_cast<char*>(pb.peer[k]) + offset;
+  o.nl = s.Nl;
+  o.H = s.H;
+  o.h0 = rank * s.Hl;
+  return o;
+}
+
+enum { kSlotFwdIn = 0, kSlotFwdOut = 1, kSlotBwdIn = 2, kSlotBwdOut = 3 };
 
 }  // namespace
 
@@ -358,8 +440,36 @@ ua_status ua_ctx_create(const unsigned char* uid, int P, int rank, int cuda_devi
   return UA_OK;
 }
 
+ua_status ua_ctx_set_a2a_mode(ua_ctx* ctx, int mode) {
+  if (!ctx) return fail(UA_ERR_INVALID_ARG, "ctx is NULL");
+  if (mode != UA_A2A_NCCL && mode != UA_A2A_PEER) return fail(UA_ERR_INVALID_ARG, "bad a2a mode %d", mode);
+  if (mode == UA_A2A_PEER) {
+    if (ctx->P == 1) return fail(UA_ERR_UNSUPPORTED, "peer all-to-all needs P > 1");
+    if (ctx->P > ua::kMaxPeers) return fail(UA_ERR_UNSUPPORTED, "peer all-to-all supports P <= %d", ua::kMaxPeers);
+    if (!ctx->flags.local) {
+      cudaStream_t s;
+      UA_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+      ua_status st = peer_ensure(ctx, ctx->flags, sizeof(int64_t) * 4 * ua::kMaxPeers, s);
+      cudaStreamDestroy(s);
+      if (st != UA_OK) return st;
+    }
+  }
+  ctx->a2a_mode = mode;
+  return UA_OK;
+}
+
+ua_status ua_ctx_get_a2a_mode(const ua_ctx* ctx, int* mode) {
+  if (!ctx || !mode) return fail(UA_ERR_INVALID_ARG, "null argument");
+  *mode = ctx->a2a_mode;
+  return UA_OK;
+}
+
 ua_status ua_ctx_destroy(ua_ctx* ctx) {
   if (!ctx) return UA_OK;
+  if (ctx->flags.local) {
+    cudaDeviceSynchronize();
+    for (auto* pb : {&ctx->flags, &ctx->fwd_in, &ctx->fwd_out, &ctx->bwd_in, &ctx->bwd_out}) peer_release(ctx, *pb);
+  }
   ncclResult_t r = ncclSuccess;
   if (ctx->comm) r = ncclCommDestroy(ctx->comm);
   for (auto& rec : ctx->pending) {
@@ -402,6 +512,48 @@ ua_status ua_ulysses_attn_fwd(ua_ctx* ctx, const void* q, const void* k, const v
     Phase ph(ctx, UA_PHASE_ATTN_FWD, stream);
     return launch_attention_fwd(q, k, v, sn, sh, sb, o, nullptr, 0, 0, 0, lse, N, int64_t(H) * N, B, N, H, D, 0, N,
                                 stream);
+  }
+
+  if (ctx->a2a_mode == UA_A2A_PEER) {
+    // Fused all-to-alls over NVLink peer stores (no NCCL on the data path).
+    const size_t S = size_t(s.shard()) * 2;
+    UA_TRY(peer_ensure(ctx, ctx->fwd_in, 3 * S, stream));   // [3][N][B][Hl][D] on every rank
+    UA_TRY(peer_ensure(ctx, ctx->fwd_out, S, stream));      // [B][Nl][H][D] token-owner output
+    const int64_t step = ++ctx->step_fwd;
+    const ua::PeerFlags fl = peer_flags(ctx);
+    {  // 1+2. pack straight into every head owner's receive buffer, then flag it
+      Phase ph(ctx, UA_PHASE_PACK_FWD, stream);
+      ua::PeerPack pk{};
+      pk.src[0] = q; pk.src[1] = k; pk.src[2] = v;
+      for (int j = 0; j < P; ++j) pk.dst[j] = ctx->fwd_in.peer[j];
+      pk.ntensors = 3;
+      UA_CUDA(ua::launch_pack_push(pk, B, s.Nl, H, D, P, ctx->rank, stream));
+      UA_CUDA(ua::launch_signal(fl, kSlotFwdIn, ctx->rank, P, step, stream));
+    }
+    {
+      Phase ph(ctx, UA_PHASE_A2A_FWD_IN, stream);
+      UA_CUDA(ua::launch_wait_copy(static_cast<const int64_t*>(ctx->flags.local), kSlotFwdIn, P, step, nullptr,
+                                   nullptr, 0, stream));
+      ctx->a2a_calls += 1;
+      ctx->a2a_bytes += int64_t(P - 1) * int64_t(s.chunk()) * 2 * 3;
+    }
+    const int64_t sn = B * int64_t(s.Hl) * D, sh = D, sb = int64_t(s.Hl) * D;
+    char* rin = static_cast<char*>(ctx->fwd_in.local);
+    const ua::PeerOut po = peer_out(ctx->fwd_out, 0, s, ctx->rank);
+    {  // 3+4. attention; the epilogue stores O rows into the token owners' buffers
+      Phase ph(ctx, UA_PHASE_ATTN_FWD, stream);
+      UA_TRY(launch_attention_fwd(rin, rin + S, rin + 2 * S, sn, sh, sb, ua::ViewArg{nullptr, 0, 0, 0}, nullptr, 0, 0,
+                                  0, lse, N, int64_t(s.Hl) * N, B, N, s.Hl, D, 0, N, stream, &po));
+      UA_CUDA(ua::launch_signal(fl, kSlotFwdOut, ctx->rank, P, step, stream));
+    }
+    {  // 5. all owners' rows are in: copy into the caller's out
+      Phase ph(ctx, UA_PHASE_UNPACK_FWD, stream);
+      UA_CUDA(ua::launch_wait_copy(static_cast<const int64_t*>(ctx->flags.local), kSlotFwdOut, P, step,
+                                   ctx->fwd_out.local, out, int64_t(S), stream));
+      ctx->a2a_calls += 1;
+      ctx->a2a_bytes += int64_t(P - 1) * int64_t(s.chunk()) * 2;
+    }
+    return UA_OK;
   }
 
   char* ws = static_cast<char*>(workspace);
@@ -483,6 +635,65 @@ ua_status ua_ulysses_attn_bwd(ua_ctx* ctx, const void* q, const void* k, const v
     {
       Phase ph(ctx, UA_PHASE_DQ_FINALIZE, stream);
       UA_CUDA(ua::launch_dq_finalize(dq_acc, vdq, B, N, H, D, scale, stream));
+    }
+    return UA_OK;
+  }
+
+  if (ctx->a2a_mode == UA_A2A_PEER) {
+    // Fused all-to-alls over NVLink peer stores (no NCCL on the data path).
+    const size_t S = size_t(s.shard()) * 2;
+    const size_t DL = size_t(B * s.Nl * H) * 4;  // Delta bytes received per rank
+    UA_TRY(peer_ensure(ctx, ctx->bwd_in, 4 * S + DL, stream));  // [4][N][B][Hl][D] + Delta [N][B][Hl]
+    UA_TRY(peer_ensure(ctx, ctx->bwd_out, 3 * S, stream));      // [3][B][Nl][H][D]: dq, dk, dv of the owner
+    const int64_t step = ++ctx->step_bwd;
+    const ua::PeerFlags fl = peer_flags(ctx);
+    {  // 1+2. q, k, v, dO + Delta straight into every head owner's receive buffer
+      Phase ph(ctx, UA_PHASE_PACK_BWD, stream);
+      ua::PeerPack pk{};
+      pk.src[0] = q; pk.src[1] = k; pk.src[2] = v; pk.src[3] = dout;
+      for (int j = 0; j < P; ++j) pk.dst[j] = ctx->bwd_in.peer[j];
+      pk.ntensors = 4;
+      pk.dout = dout;
+      pk.out = out;
+      UA_CUDA(ua::launch_pack_push(pk, B, s.Nl, H, D, P, ctx->rank, stream));
+      UA_CUDA(ua::launch_signal(fl, kSlotBwdIn, ctx->rank, P, step, stream));
+    }
+    {
+      Phase ph(ctx, UA_PHASE_A2A_BWD_IN, stream);
+      UA_CUDA(ua::launch_wait_copy(static_cast<const int64_t*>(ctx->flags.local), kSlotBwdIn, P, step, nullptr,
+                                   nullptr, 0, stream));
+      ctx->a2a_calls += 1;
+      ctx->a2a_bytes += int64_t(P - 1) * (int64_t(s.chunk()) * 2 * 4 + int64_t(s.Nl * B * s.Hl) * 4);
+    }
+    char* rin = static_cast<char*>(ctx->bwd_in.local);
+    const float* rdelta = reinterpret_cast<const float*>(rin + 4 * S);
+    float* dq_acc = reinterpret_cast<float*>(ws + plan.dq_acc);
+    const int64_t sn = B * int64_t(s.Hl) * D, sh = D, sb = int64_t(s.Hl) * D;
+    const ua::PeerOut pdq = peer_out(ctx->bwd_out, 0, s, ctx->rank);
+    const ua::PeerOut pdk = peer_out(ctx->bwd_out, S, s, ctx->rank);
+    const ua::PeerOut pdv = peer_out(ctx->bwd_out, 2 * S, s, ctx->rank);
+    {  // 3. attention backward; dK, dV rows go straight to the token owners
+      Phase ph(ctx, UA_PHASE_ATTN_BWD, stream);
+      UA_CUDA(cudaMemsetAsync(dq_acc, 0, size_t(B * s.Hl * n_pad * D) * 4, stream));
+      ua::ViewArg none{nullptr, 0, 0, 0};
+      UA_TRY(launch_attention_bwd(rin, rin + S, rin + 2 * S, rin + 3 * S, sn, sh, sb, none, none, dq_acc, lse, N,
+                                  int64_t(s.Hl) * N, rdelta, B * int64_t(s.Hl), 1, s.Hl, B, N, s.Hl, D,
+                                  reinterpret_cast<float2*>(ws + plan.lsed), stream, &pdk, &pdv));
+    }
+    {  // 4. dq = bf16(scale * dq_acc) into the token owners' buffers, then flag
+      Phase ph(ctx, UA_PHASE_DQ_FINALIZE, stream);
+      UA_CUDA(ua::launch_finalize_push(dq_acc, pdq, B, N, s.Hl, D, scale, stream));
+      UA_CUDA(ua::launch_signal(fl, kSlotBwdOut, ctx->rank, P, step, stream));
+    }
+    {  // 5. all heads' rows are in: copy into the caller's dq, dk, dv
+      Phase ph(ctx, UA_PHASE_UNPACK_BWD, stream);
+      char* rout = static_cast<char*>(ctx->bwd_out.local);
+      UA_CUDA(ua::launch_wait_copy(static_cast<const int64_t*>(ctx->flags.local), kSlotBwdOut, P, step, rout, dq,
+                                   int64_t(S), stream));
+      UA_CUDA(cudaMemcpyAsync(dk, rout + S, S, cudaMemcpyDeviceToDevice, stream));
+      UA_CUDA(cudaMemcpyAsync(dv, rout + 2 * S, S, cudaMemcpyDeviceToDevice, stream));
+      ctx->a2a_calls += 1;
+      ctx->a2a_bytes += int64_t(P - 1) * int64_t(s.chunk()) * 2 * 3;
     }
     return UA_OK;
   }

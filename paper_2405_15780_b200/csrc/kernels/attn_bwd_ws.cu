@@ -370,6 +370,11 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_ws_kernel(const __grid_consta
       const float sc = hh == 0 ? 1.f : p.scale;
       __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(dst_v.base) + b * dst_v.sb + h * dst_v.sh +
                            int64_t(krow) * dst_v.sn;
+      const PeerOut& po = hh == 0 ? p.dv_peer : p.dk_peer;
+      if (po.base[0] != nullptr && valid) {  // fused return all-to-all: the token owner's buffer
+        const int owner = int(krow / po.nl);
+        dst = reinterpret_cast<__nv_bfloat16*>(po.base[owner]) + ((b * po.nl + (krow - owner * po.nl)) * po.H + po.h0 + h) * D;
+      }
 #pragma unroll
       for (int cc = 0; cc < D; cc += 16) {
         uint32_t r[16];

@@ -399,6 +399,11 @@ __global__ void __launch_bounds__(384, 1) attn_fwd_kernel(const __grid_constant_
     const float inv_l = 1.f / l;
     const bool valid = q_row < p.n_q;
     __nv_bfloat16* orow = reinterpret_cast<__nv_bfloat16*>(p.o.base) + b * p.o.sb + h * p.o.sh + int64_t(q_row) * p.o.sn;
+    if (p.o_peer.base[0] != nullptr && valid) {  // fused return all-to-all: store into the token owner's buffer
+      const int owner = int(q_row / p.o_peer.nl);
+      orow = reinterpret_cast<__nv_bfloat16*>(p.o_peer.base[owner]) +
+             ((b * p.o_peer.nl + (q_row - owner * p.o_peer.nl)) * p.o_peer.H + p.o_peer.h0 + h) * D;
+    }
 #pragma unroll
     for (int cc = 0; cc < D; cc += 32) {
       uint32_t r[32];

@@ -13,11 +13,34 @@ struct ViewArg {
   int64_t sn, sh, sb;  // element strides of token, head, batch (d contiguous)
 };
 
+// ---- NVLink peer-store all-to-all (peer.cu) -----------------------------------
+constexpr int kMaxPeers = 8;
+// Token-owner output buffers: rank k's base[k] is a [B][nl][H][D] bf16 tensor
+// (CUDA IPC mapping); a head-shard row (b, global token n, local head h) goes to
+// base[n / nl] at ((b*nl + n % nl)*H + h0 + h)*D.  base[0] == nullptr: unused.
+struct PeerOut {
+  void* base[kMaxPeers];
+  int64_t nl;
+  int H;
+  int h0;
+};
+struct PeerPack {
+  const void* src[4];     // local shards [B][Nl][H][D]
+  void* dst[kMaxPeers];   // each rank's receive buffer: [ntensors][N][B][Hl][D] (+ Delta [N][B][Hl] fp32)
+  int ntensors;
+  const void* dout;       // non-null: also push Delta = rowsum(dout * out)
+  const void* out;
+};
+struct PeerFlags {
+  int64_t* peer[kMaxPeers];  // every rank's flag array [4 slots][kMaxPeers]
+};
+
 struct alignas(64) FwdParams {
   CUtensorMap tm_q;  // 4-D maps {D, N, heads, B} over the Q / K / V views
   CUtensorMap tm_k;
   CUtensorMap tm_v;
-  ViewArg o;          // bf16 output (used when o_f32 == nullptr)
+  ViewArg o;          // bf16 output (used when o_f32 == nullptr and o_peer.base[0] == nullptr)
+  PeerOut o_peer;     // peer mode: O rows straight into the token owner's buffer
   float* o_f32;       // optional fp32 normalised output (LSS segments)
   int64_t of_sn, of_sh, of_sb;
   float* lse;         // lse[b*l_sb + h*l_sh + n]
@@ -35,7 +58,8 @@ struct alignas(64) BwdParams {
   CUtensorMap tm_dq;  // fp32 2-D {D, B*heads*N_pad} over dq_acc, box {32, 128}, SW128 (reduce-add target)
   CUtensorMap tm_qh;  // Q / dO with 64-row boxes (half-tile ring of the ws kernel)
   CUtensorMap tm_doh;
-  ViewArg dk, dv;     // bf16 outputs
+  ViewArg dk, dv;     // bf16 outputs (used when dk_peer.base[0] == nullptr)
+  PeerOut dk_peer, dv_peer;  // peer mode: dK, dV rows straight into the token owner's buffers
   float* dq_acc;      // fp32 [B*heads][N_pad][D] accumulator, N_pad = ceil(N/128)*128 (zeroed by caller)
   const float* lse;   // lse[b*l_sb + h*l_sh + n]
   int64_t l_sh, l_sb;
@@ -74,6 +98,14 @@ cudaError_t launch_dq_finalize(const float* dq_acc, ViewArg dq, int64_t B, int64
 cudaError_t launch_bwd_prep(const float* lse, int64_t l_sh, int64_t l_sb, const float* delta, int64_t d_sn,
                             int64_t d_sh, int64_t d_sb, float2* lsed, int64_t B, int heads, int64_t N,
                             cudaStream_t stream);
+// Peer all-to-all pieces (peer.cu).
+cudaError_t launch_pack_push(const PeerPack& pk, int64_t B, int64_t Nl, int H, int D, int P, int rank,
+                             cudaStream_t stream);
+cudaError_t launch_signal(const PeerFlags& f, int slot, int rank, int P, int64_t step, cudaStream_t stream);
+cudaError_t launch_wait_copy(const int64_t* flags, int slot, int P, int64_t step, const void* src, void* dst,
+                             int64_t bytes, cudaStream_t stream);
+cudaError_t launch_finalize_push(const float* dq_acc, const PeerOut& o, int64_t B, int64_t N, int heads, int D,
+                                 float scale, cudaStream_t stream);
 // Exact merge of two LSS segment results (in place into a):
 //   lse = logaddexp(lse_a, lse_b); O = e^{lse_a-lse} O_a + e^{lse_b-lse} O_b
 cudaError_t launch_lse_merge(float* o_a, float* lse_a, const float* o_b, const float* lse_b, int64_t rows, int D,

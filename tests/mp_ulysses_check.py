@@ -31,6 +31,7 @@ def main():
     ap.add_argument("--H", type=int, default=8)
     ap.add_argument("--D", type=int, default=64)
     ap.add_argument("--sigma", type=float, default=1.0)
+    ap.add_argument("--mode", default="nccl", choices=["nccl", "peer"])
     a = ap.parse_args()
     rank, P = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
@@ -44,6 +45,8 @@ def main():
     qs, ks, vs, ds = (t[:, sl].contiguous().to(dev) for t in (q, k, v, do))
 
     ctx = ua.Context(P=P, rank=rank, device=local)
+    ctx.set_a2a_mode(a.mode)
+    assert ctx.a2a_mode() == a.mode
     # head limit: every rank must get the same error, before any collective
     try:
         ua.ulysses_attn_fwd(ctx, *(torch.zeros(1, 4, 1, D, dtype=torch.bfloat16, device=dev) for _ in range(3)))
@@ -63,6 +66,13 @@ def main():
     assert c1 - c0 == 2 and c2 - c1 == 2, (c0, c1, c2)
     exp_f = 4 * Nl * H * D * 2 * (P - 1) // P          # q,k,v in + o out, off-rank
     assert bytes_f == exp_f, (bytes_f, exp_f)
+    # a second step reuses the (peer) buffers and flag counters: same bits
+    r2 = ua.ulysses_attn_fwd(ctx, qs, ks, vs)
+    dq2, dk2, dv2 = ua.ulysses_attn_bwd(ctx, qs, ks, vs, r2.out, r2.lse, ds)
+    torch.cuda.synchronize()
+    assert torch.equal(r2.out, r.out) and torch.equal(r2.lse, r.lse)
+    assert torch.equal(dk2, dk) and torch.equal(dv2, dv)
+    assert (dq2.float() - dq.float()).abs().max().item() <= 2e-2
 
     def gather(t):
         parts = [torch.empty_like(t) for _ in range(P)]

@@ -21,6 +21,7 @@ def torchrun(nproc, script, *args, timeout=900, env=None):
 
 # ----------------------------------------------------------------- GPU, NCCL
 @pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["nccl", "peer"])
 @pytest.mark.parametrize("P,N,H,D,sigma", [
     (2, 4096, 8, 64, 1.0),
     (2, 2048, 4, 128, 2.0),
@@ -29,11 +30,11 @@ def torchrun(nproc, script, *args, timeout=900, env=None):
     (8, 8192, 16, 64, 1.0),
     (8, 2048, 8, 32, 2.0),
 ])
-def test_ulysses_p_way(P, N, H, D, sigma):
+def test_ulysses_p_way(P, N, H, D, sigma, mode):
     if torch.cuda.device_count() < P:
         pytest.skip(f"needs {P} GPUs")
     r = torchrun(P, os.path.join(ROOT, "tests", "mp_ulysses_check.py"), f"--N={N}", f"--H={H}", f"--D={D}",
-                 f"--sigma={sigma}")
+                 f"--sigma={sigma}", f"--mode={mode}")
     assert r.returncode == 0 and "MP_OK" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
 
 
