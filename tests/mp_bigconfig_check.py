@@ -33,6 +33,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="c4")
     ap.add_argument("--rows", type=int, default=4, help="random rows per rank (plus boundary rows)")
+    ap.add_argument("--mode", default="nccl", choices=["nccl", "peer"])
     a = ap.parse_args()
     cfg = synth.CONFIGS[a.config]
     B, N, H, D = cfg["B"], cfg["N"], cfg["H"], cfg["D"]
@@ -47,6 +48,8 @@ def main():
     qs, ks, vs, ds = (t.to(dev) for t in (q, k, v, do))
 
     ctx = ua.Context(P=P, rank=rank, device=local)
+    if P > 1:
+        ctx.set_a2a_mode(a.mode)
     c0, _ = ctx.comm_stats()
     r = ua.ulysses_attn_fwd(ctx, qs, ks, vs)
     dq, dk, dv = ua.ulysses_attn_bwd(ctx, qs, ks, vs, r.out, r.lse, ds)

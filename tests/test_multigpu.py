@@ -40,13 +40,18 @@ def test_ulysses_p_way(P, N, H, D, sigma, mode):
 
 @pytest.mark.gpu
 @pytest.mark.slow
-@pytest.mark.parametrize("config,P", [("c3", 1), ("c4", 1), ("c3", 2), ("c3", 4), ("c3", 8), ("c4", 2), ("c4", 4), ("c4", 8),
-                                      ("c5", 4), ("c5", 8)])
-def test_bigconfig_p_way(config, P):
+@pytest.mark.parametrize("config,P,mode", [("c3", 1, "nccl"), ("c4", 1, "nccl"),
+                                           ("c3", 2, "nccl"), ("c3", 4, "nccl"), ("c3", 8, "nccl"),
+                                           ("c4", 2, "nccl"), ("c4", 4, "nccl"), ("c4", 8, "nccl"),
+                                           ("c5", 4, "nccl"), ("c5", 8, "nccl"),
+                                           ("c3", 4, "peer"), ("c4", 4, "peer"), ("c5", 4, "peer"),
+                                           ("c4", 8, "peer"), ("c5", 8, "peer")])
+def test_bigconfig_p_way(config, P, mode):
     """BASELINE configs at full size: sampled-row oracle parity + invariants."""
     if torch.cuda.device_count() < P:
         pytest.skip(f"needs {P} GPUs")
-    r = torchrun(P, os.path.join(ROOT, "tests", "mp_bigconfig_check.py"), f"--config={config}", timeout=1500)
+    r = torchrun(P, os.path.join(ROOT, "tests", "mp_bigconfig_check.py"), f"--config={config}", f"--mode={mode}",
+                 timeout=1500)
     assert r.returncode == 0 and "BIG_OK" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
 
 
