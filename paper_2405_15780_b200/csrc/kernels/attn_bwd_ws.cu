@@ -28,6 +28,7 @@
 //   drain (the S^T GEMMs of the next tile run meanwhile).
 #include "attn_common.cuh"
 #include "attn_kernels.h"
+#include "trace.cuh"
 
 #ifndef UA_BWD_POLY_MOD
 #define UA_BWD_POLY_MOD 4   // every UA_BWD_POLY_MOD-th exp2 pair on the FMA pipe (0: none)
@@ -155,7 +156,9 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_ws_kernel(const __grid_consta
           const float* lsed_tile = lsed_bh + int64_t(tile) * 256;  // [128 nl][128 nd]
           for (int hh = 0; hh < 2; ++hh) {
             const int U = 2 * T + hh, s = U % kSl;
+            UA_TEV(0, U, 1);
             if (U >= kSl) mbar_wait(&slot_empty[s], ((U / kSl) & 1) ^ 1);
+            UA_TEV(0, U, 2);
             mbar_arrive_expect_tx(&slot_full[s], C::kSlotBytes + C::kLsedBytes);
             for (int a = 0; a < G::kAtoms; ++a) {
               tma_load_4d(qslot(s) + a * 64 * G::kSw, &p.tm_qh, &slot_full[s], a * G::kAtomCols, tile * 128 + 64 * hh,
@@ -231,7 +234,9 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_ws_kernel(const __grid_consta
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {
             const int U = 2 * T + hh;
+            UA_TEV(1, T, 1 + 4 * hh);
             mbar_wait(&ds_ready[hh], T & 1);
+            UA_TEV(1, T, 2 + 4 * hh);
             tc_fence_after();
             const uint32_t acc = (t > 0 || hh > 0) ? 1u : 0u;
 #pragma unroll
@@ -243,9 +248,12 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_ws_kernel(const __grid_consta
               mma_ts(tbase + C::kColDK, tbase + C::kColDP + 64 * hh + kk * 8, mnmajor_desc_r<D, 64>(q_at(U), kk),
                      idesc_g, (acc || kk > 0) ? 1u : 0u);
             mma_commit(&slot_empty[U % kSl]);
+            UA_TEV(1, T, 3 + 4 * hh);
             if (hh == 1) {  // dQ(T) = dS K
               if (!C::kAliasDq && T > 0) {
+                UA_TEV(1, T, 9);
                 mbar_wait(dq_empty, (T - 1) & 1);
+                UA_TEV(1, T, 10);
                 tc_fence_after();
               }
               const uint32_t ds = sdSa + (T % C::kNumDs) * C::kDsBytes;
@@ -254,6 +262,7 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_ws_kernel(const __grid_consta
                 mma_ss(tbase + C::kColDQ, mnmajor_desc_r<128, 128>(ds, kk), mnmajor_desc_r<D, 128>(sKa, kk), idesc_q,
                        kk > 0 ? 1u : 0u);
               mma_commit(dq_full);
+              UA_TEV(1, T, 11);
               mma_commit(&ds_free[T % C::kNumDs]);
             }
             if (t + 1 < n_q) {  // next tile, this half
@@ -315,9 +324,11 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_ws_kernel(const __grid_consta
       }
       for (int t = 0; t < n_q; ++t, ++T) {
         const int U = 2 * T + hh, s = U % kSl;
+        if (j == 0) UA_TEV(2 + hh, T, 1);
         mbar_wait(&slot_full[s], (U / kSl) & 1);  // (lse, Delta) of this half landed
         if (T >= C::kNumDs) mbar_wait(&ds_free[T % C::kNumDs], ((T / C::kNumDs) & 1) ^ 1);
         mbar_wait(&sdp_full[hh], T & 1);
+        if (j == 0) UA_TEV(2 + hh, T, 2);
         tc_fence_after();
         uint8_t* atom = sdS + (T % C::kNumDs) * C::kDsBytes + hh * (128 * 128) + j * 128;
         const float4* nl4 = reinterpret_cast<const float4*>(sLsed + s * 128);
@@ -358,6 +369,7 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_ws_kernel(const __grid_consta
         fence_proxy_async_smem();
         tmem_st_wait();
         tc_fence_before();
+        if (j == 0) UA_TEV(2 + hh, T, 3);
         mbar_arrive(&ds_ready[hh]);
       }
       // ------------------------------------------------ dV (hh=0) / dK (hh=1) epilogue
@@ -404,7 +416,9 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_ws_kernel(const __grid_consta
       const int bh = item / n_kt;
       for (int t = 0; t < n_q; ++t, ++T) {
         const int tile = (start + t) % n_q;
+        if (r == 0) UA_TEV(4, T, 1);
         mbar_wait(dq_full, T & 1);
+        if (r == 0) UA_TEV(4, T, 2);
         tc_fence_after();
 #pragma unroll
         for (int rd = 0; rd < kRounds; ++rd) {
@@ -420,6 +434,7 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_ws_kernel(const __grid_consta
           if (rd == kRounds - 1) {
             tc_fence_before();
             mbar_arrive(dq_empty);
+            if (r == 0) UA_TEV(4, T, 3);
           }
           // kCols / 32 boxes through kStageBoxes staging boxes
 #pragma unroll
@@ -471,7 +486,13 @@ cudaError_t launch_bwd_ws_impl(const BwdParams& p, cudaStream_t stream) {
   }
   const int64_t items = int64_t(p.batch) * p.heads * ((p.n + 127) / 128);
   const int grid = int(items < num_sms ? items : num_sms);
+#if UA_TRACE
+  trace_reset();
+#endif
   attn_bwd_ws_kernel<D><<<grid, C::kThreads, C::kSmemBytes, stream>>>(p);
+#if UA_TRACE
+  trace_dump("bwd");
+#endif
   return cudaGetLastError();
 }
 
