@@ -334,11 +334,21 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_ws_kernel(const __grid_consta
         const float4* nl4 = reinterpret_cast<const float4*>(sLsed + s * 128);
         const float4* nd4 = reinterpret_cast<const float4*>(sLsed + s * 128 + 64);
 #pragma unroll
+        // TMEM loads software-pipelined: chunk k+1's S^T / dP^T columns are in
+        // flight while chunk k is computed (P^T / dS^T stores only ever touch
+        // columns already read).
+        uint32_t rsA[16], rdA[16], rsB[16], rdB[16];
+        tmem_ld16(t_lane + colS, rsA);
+        tmem_ld16(t_lane + colDP, rdA);
+        tmem_ld_wait();
+#pragma unroll
         for (int cc = 0; cc < 64; cc += 16) {
-          uint32_t rs[16], rd[16];
-          tmem_ld16(t_lane + colS + cc, rs);
-          tmem_ld16(t_lane + colDP + cc, rd);
-          tmem_ld_wait();
+          uint32_t* rs = ((cc / 16) & 1) ? rsB : rsA;
+          uint32_t* rd = ((cc / 16) & 1) ? rdB : rdA;
+          if (cc + 16 < 64) {
+            tmem_ld16(t_lane + colS + cc + 16, ((cc / 16) & 1) ? rsA : rsB);
+            tmem_ld16(t_lane + colDP + cc + 16, ((cc / 16) & 1) ? rdA : rdB);
+          }
           uint32_t pk_p[8], pk_ds[8];
 #pragma unroll
           for (int x = 0; x < 16; x += 4) {
@@ -365,6 +375,7 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_ws_kernel(const __grid_consta
             *reinterpret_cast<uint4*>(atom + chunk * 16) =
                 make_uint4(pk_ds[4 * qd], pk_ds[4 * qd + 1], pk_ds[4 * qd + 2], pk_ds[4 * qd + 3]);
           }
+          if (cc + 16 < 64) tmem_ld_wait();
         }
         fence_proxy_async_smem();
         tmem_st_wait();
