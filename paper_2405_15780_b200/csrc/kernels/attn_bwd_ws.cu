@@ -330,9 +330,9 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_ws_kernel(const __grid_consta
         mbar_wait(&sdp_full[hh], T & 1);
         if (j == 0) UA_TEV(2 + hh, T, 2);
         tc_fence_after();
-        uint8_t* atom = sdS + (T % C::kNumDs) * C::kDsBytes + hh * (128 * 128) + j * 128;
-        const float4* nl4 = reinterpret_cast<const float4*>(sLsed + s * 128);
-        const float4* nd4 = reinterpret_cast<const float4*>(sLsed + s * 128 + 64);
+        const uint32_t atom = smem_u32(sdS + (T % C::kNumDs) * C::kDsBytes + hh * (128 * 128) + j * 128);
+        const uint32_t nl_s = smem_u32(sLsed + s * 128);
+        const uint32_t nd_s = nl_s + 64 * 4;
 #pragma unroll
         // TMEM loads software-pipelined: chunk k+1's S^T / dP^T columns are in
         // flight while chunk k is computed (P^T / dS^T stores only ever touch
@@ -352,8 +352,8 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_ws_kernel(const __grid_consta
           uint32_t pk_p[8], pk_ds[8];
 #pragma unroll
           for (int x = 0; x < 16; x += 4) {
-            const float4 nl = nl4[(cc + x) / 4];
-            const float4 nd = nd4[(cc + x) / 4];
+            const float4 nl = lds128(nl_s + (cc + x) * 4);
+            const float4 nd = lds128(nd_s + (cc + x) * 4);
 #pragma unroll
             for (int u = 0; u < 2; ++u) {
               const float2 arg = __ffma2_rn(make_float2(__uint_as_float(rs[x + 2 * u]), __uint_as_float(rs[x + 2 * u + 1])),
@@ -372,8 +372,7 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_ws_kernel(const __grid_consta
 #pragma unroll
           for (int qd = 0; qd < 2; ++qd) {
             const int chunk = ((cc / 8) + qd) ^ (j & 7);
-            *reinterpret_cast<uint4*>(atom + chunk * 16) =
-                make_uint4(pk_ds[4 * qd], pk_ds[4 * qd + 1], pk_ds[4 * qd + 2], pk_ds[4 * qd + 3]);
+            sts128(atom + chunk * 16, pk_ds[4 * qd], pk_ds[4 * qd + 1], pk_ds[4 * qd + 2], pk_ds[4 * qd + 3]);
           }
           if (cc + 16 < 64) tmem_ld_wait();
         }
@@ -454,12 +453,11 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_ws_kernel(const __grid_consta
             named_bar_sync(1, 128);
 #pragma unroll
             for (int sb = 0; sb < C::kStageBoxes; ++sb) {
-              uint8_t* srow = sStage + sb * C::kBoxBytes + r * 128;
+              const uint32_t srow = smem_u32(sStage + sb * C::kBoxBytes + r * 128);
 #pragma unroll
               for (int q4 = 0; q4 < 8; ++q4) {
                 const int e = 32 * (cb0 + sb) + 4 * q4;
-                *reinterpret_cast<float4*>(srow + ((q4 ^ (r & 7)) * 16)) =
-                    make_float4(acc[e], acc[e + 1], acc[e + 2], acc[e + 3]);
+                sts128f(srow + ((q4 ^ (r & 7)) * 16), acc[e], acc[e + 1], acc[e + 2], acc[e + 3]);
               }
             }
             fence_proxy_async_smem();
