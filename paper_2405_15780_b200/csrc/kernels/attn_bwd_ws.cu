@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_ws_kernel(const __grid_consta
   using G = TileGeom<D>;
   constexpr int kSl = C::kSlots;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // 1024-B aligned, stays in the shared window
   uint8_t* sK = smem;
   uint8_t* sV = sK + G::kTileBytes;
   uint8_t* sSlots = sV + G::kTileBytes;                        // [kSl] { Q_h, dO_h }

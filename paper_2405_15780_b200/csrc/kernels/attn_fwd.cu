@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(384, 1) attn_fwd_kernel(const __grid_constant_
   using G = TileGeom<D>;
   constexpr int kStages = C::kStages;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // 1024-B aligned, stays in the shared window
   uint8_t* sQ = smem;                                  // [2] tiles
   uint8_t* sK = sQ + 2 * G::kTileBytes;                // [kStages]
   uint8_t* sV = sK + kStages * G::kTileBytes;          // [kStages]
