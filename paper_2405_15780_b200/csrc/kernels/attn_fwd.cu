@@ -15,11 +15,14 @@
 //      warp 1      tcgen05.mma issuer (single elected thread) + TMEM owner
 //      warps 4-7   softmax for query tile 0 (one row per thread)
 //      warps 8-11  softmax for query tile 1
-//  * TMEM (512 cols): S0 [0,128) S1 [128,256) O0 [256,256+D) O1 [256+D, 256+2D).
-//    S_t = Q_t K_j^T (SS MMA, M=128,N=128,K=D).  The softmax rewrites S_t in
-//    place as bf16 P_t (64 cols, packed pairs) and O_t += P_t V_j runs as a TS
-//    MMA (A = P from TMEM, B = V from smem, MN-major).  The two tiles ping-pong:
-//    while tile 0 does its softmax the tensor core runs tile 1's GEMMs.
+//  * TMEM (512 cols), D <= 64: S0 S1 [0,256) | P0 P1 [256,384) | O0 O1 [384,512).
+//    S_t = Q_t K_j^T (SS MMA, M=128,N=128,K=D).  The softmax loads S_t into
+//    registers and releases it (s_free), so S_t(j+1) is computed while it
+//    exponentiates; it writes bf16 P_t (64 cols, packed pairs) and
+//    O_t += P_t V_j runs as a TS MMA (A = P from TMEM, B = V from smem,
+//    MN-major).  D = 128 has no room for separate P: S0 S1 | O0 O1, P
+//    overwrites S_t in place and the two tiles ping-pong (one tile's GEMMs
+//    under the other tile's softmax).
 //  * online softmax in the log2 domain with a lazy max: the running max m used
 //    for the exponent is only raised (and O, l rescaled) when a row's max grows
 //    by more than 8 (a factor 256); the final o = O / l is exact either way
@@ -31,13 +34,16 @@
 // Tuning knobs (defaults are the shipped configuration; scripts/ab.py builds
 // variants with -D overrides).
 #ifndef UA_FWD_SEP_P
-#define UA_FWD_SEP_P 0      // separate TMEM P buffers when D <= 64 (A/B: slower, kept as an option)
+#define UA_FWD_SEP_P 1      // separate TMEM P buffers when D <= 64: the next Q K^T overlaps this tile's softmax
 #endif
 #ifndef UA_FWD_POLY_MOD
 #define UA_FWD_POLY_MOD 3   // every UA_FWD_POLY_MOD-th exp2 pair on the FMA pipe (0: none)
 #endif
 #ifndef UA_FWD_PINGPONG
 #define UA_FWD_PINGPONG 0   // the two softmax warpgroups take turns for their exp2 phases (A/B: slower)
+#endif
+#ifndef UA_FWD_LDBATCH
+#define UA_FWD_LDBATCH 1    // issue the four S chunk loads back to back with one wait
 #endif
 #ifndef UA_FWD_RELOAD
 #define UA_FWD_RELOAD 0     // two TMEM passes over S (max, then exp); A/B: slower, kept as an option
@@ -46,6 +52,16 @@
 namespace ua {
 
 namespace {
+
+#ifndef UA_FWD_POLY16
+#define UA_FWD_POLY16 6     // >0: this many of every 16 exp2 pairs on the FMA pipe, spread evenly (overrides POLY_MOD)
+#endif
+
+// Which of the 16 exp2 pairs of a 32-column chunk go to the FMA-pipe polynomial.
+__device__ __forceinline__ constexpr bool poly_pair(int i) {
+  if (UA_FWD_POLY16 > 0) return ((i + 1) * UA_FWD_POLY16) / 16 - (i * UA_FWD_POLY16) / 16 == 1;
+  return UA_FWD_POLY_MOD > 0 && (i % (UA_FWD_POLY_MOD > 0 ? UA_FWD_POLY_MOD : 1)) == 1;
+}
 
 template <int D>
 struct FwdCfg {
@@ -277,6 +293,16 @@ __global__ void __launch_bounds__(384, 1) attn_fwd_kernel(const __grid_constant_
       }
 #else
       float sv[128];
+#if UA_FWD_LDBATCH
+      {  // all four 32-column loads in flight, one wait
+        uint32_t r[128];
+#pragma unroll
+        for (int cc = 0; cc < 128; cc += 32) tmem_ld32(t_lane + colS + cc, r + cc);
+        tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 128; ++i) sv[i] = __uint_as_float(r[i]);
+      }
+#else
 #pragma unroll
       for (int cc = 0; cc < 128; cc += 32) {
         uint32_t r[32];
@@ -285,6 +311,7 @@ __global__ void __launch_bounds__(384, 1) attn_fwd_kernel(const __grid_constant_
 #pragma unroll
         for (int i = 0; i < 32; ++i) sv[cc + i] = __uint_as_float(r[i]);
       }
+#endif
       if constexpr (C::kSeparateP) {  // S_t is in registers: the next Q K^T may overwrite it
         tc_fence_before();
         mbar_arrive(&s_free[t]);
@@ -340,7 +367,7 @@ __global__ void __launch_bounds__(384, 1) attn_fwd_kernel(const __grid_constant_
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
           const float2 x = __ffma2_rn(make_float2(__uint_as_float(cur[2 * i]), __uint_as_float(cur[2 * i + 1])), c2, nm2);
-          const bool poly = C::kPolyExp && UA_FWD_POLY_MOD > 0 && (i % (UA_FWD_POLY_MOD > 0 ? UA_FWD_POLY_MOD : 1)) == 1;
+          const bool poly = C::kPolyExp && poly_pair(i);
           const float2 pp = poly ? exp2_poly2(x) : make_float2(ex2(x.x), ex2(x.y));
           ls[i & 1] = __fadd2_rn(ls[i & 1], pp);
           pk[i] = pack_bf16x2(pp.x, pp.y);
@@ -360,7 +387,7 @@ __global__ void __launch_bounds__(384, 1) attn_fwd_kernel(const __grid_constant_
         for (int i = 0; i < 16; ++i) {
           const float2 x = __ffma2_rn(make_float2(sv[cc + 2 * i], sv[cc + 2 * i + 1]), c2, nm2);
           // a third of the pairs on the FMA pipe when the exp unit co-binds (D <= 64)
-          const bool poly = C::kPolyExp && UA_FWD_POLY_MOD > 0 && (i % (UA_FWD_POLY_MOD > 0 ? UA_FWD_POLY_MOD : 1)) == 1;
+          const bool poly = C::kPolyExp && poly_pair(i);
           const float2 pp = poly ? exp2_poly2(x) : make_float2(ex2(x.x), ex2(x.y));
           ls[i & 1] = __fadd2_rn(ls[i & 1], pp);
           pk[i] = pack_bf16x2(pp.x, pp.y);
