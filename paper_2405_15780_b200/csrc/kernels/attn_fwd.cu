@@ -45,6 +45,12 @@
 #ifndef UA_FWD_LDBATCH
 #define UA_FWD_LDBATCH 1    // issue the four S chunk loads back to back with one wait
 #endif
+#ifndef UA_FWD_LATEP
+#define UA_FWD_LATEP 0      // separate-P mode: exponentiate the whole tile before waiting for the P buffer
+#endif
+#ifndef UA_FWD_MAXNREG
+#define UA_FWD_MAXNREG 224  // >0: setmaxnreg the softmax warpgroups up to this many registers (0: off)
+#endif
 #ifndef UA_FWD_RELOAD
 #define UA_FWD_RELOAD 0     // two TMEM passes over S (max, then exp); A/B: slower, kept as an option
 #endif
@@ -54,7 +60,7 @@ namespace ua {
 namespace {
 
 #ifndef UA_FWD_POLY16
-#define UA_FWD_POLY16 6     // >0: this many of every 16 exp2 pairs on the FMA pipe, spread evenly (overrides POLY_MOD)
+#define UA_FWD_POLY16 4     // >0: this many of every 16 exp2 pairs on the FMA pipe, spread evenly (overrides POLY_MOD)
 #endif
 
 // Which of the 16 exp2 pairs of a 32-column chunk go to the FMA-pipe polynomial.
@@ -131,8 +137,20 @@ __global__ void __launch_bounds__(384, 1) attn_fwd_kernel(const __grid_constant_
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
 
+#if UA_FWD_MAXNREG > 0
+  // Registers to the softmax warpgroups (the producer / MMA warpgroup needs few);
+  // each role branch re-balances first thing so ptxas sees which limit applies.
+  constexpr int kRegsLow = ((65536 / 384 / 8 * 8) * 384 - 256 * UA_FWD_MAXNREG) / 128 / 8 * 8;
+#define UA_FWD_REGS_LOW() setmaxnreg_dec<kRegsLow>()
+#define UA_FWD_REGS_HIGH() setmaxnreg_inc<UA_FWD_MAXNREG>()
+#else
+#define UA_FWD_REGS_LOW() ((void)0)
+#define UA_FWD_REGS_HIGH() ((void)0)
+#endif
+
   if (warp == 0) {
     // ------------------------------------------------------------ producer
+    UA_FWD_REGS_LOW();
     if (elect_one()) {
       tma_prefetch_desc(&p.tm_q);
       tma_prefetch_desc(&p.tm_k);
@@ -161,6 +179,7 @@ __global__ void __launch_bounds__(384, 1) attn_fwd_kernel(const __grid_constant_
     __syncwarp();
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
+    UA_FWD_REGS_LOW();
     if (elect_one()) {
       const uint32_t idesc_s = idesc_bf16_f32(128, 128, false, false);
       const uint32_t idesc_o = idesc_bf16_f32(128, D, false, true);
@@ -190,19 +209,24 @@ __global__ void __launch_bounds__(384, 1) attn_fwd_kernel(const __grid_constant_
         issue_s(0, 0);
         issue_s(1, 0);
         for (int j = 0; j < n_kv; ++j) {
+          UA_TEV(1, j, 1);
           if (j + 1 < n_kv) {
             mbar_wait(&k_full[(j + 1) % kStages], ((j + 1) / kStages) & 1);
+            UA_TEV(1, j, 2);
             for (int t = 0; t < 2; ++t) {
               mbar_wait(&s_free[t], j & 1);
               tc_fence_after();
               issue_s(t, j + 1);
+              UA_TEV(1, j, 3 + t);
             }
           }
           mbar_wait(&v_full[j % kStages], (j / kStages) & 1);
+          UA_TEV(1, j, 5);
           for (int t = 0; t < 2; ++t) {
             mbar_wait(&p_full[t], j & 1);
             tc_fence_after();
             issue_pv(t, j);
+            UA_TEV(1, j, 6 + t);
           }
           mma_commit(&kv_empty[j % kStages]);
         }
@@ -246,6 +270,7 @@ __global__ void __launch_bounds__(384, 1) attn_fwd_kernel(const __grid_constant_
     __syncwarp();
   } else if (warp >= 4) {
     // ------------------------------------------------------------ softmax
+    UA_FWD_REGS_HIGH();
     const int t = (warp - 4) / 4;
     const int quad = warp % 4;                 // TMEM lane quadrant of this warp
     const int row = quad * 32 + lane;          // row within the query tile
@@ -316,6 +341,7 @@ __global__ void __launch_bounds__(384, 1) attn_fwd_kernel(const __grid_constant_
         tc_fence_before();
         mbar_arrive(&s_free[t]);
       }
+      if (row == 0) UA_TEV(2 + t, j, 3);
       if (tail) {
 #pragma unroll
         for (int i = 0; i < 128; ++i)
@@ -341,13 +367,15 @@ __global__ void __launch_bounds__(384, 1) attn_fwd_kernel(const __grid_constant_
       }
       // p = 2^(s*c - m): packed fp32x2 FFMA for the argument, MUFU ex2 or the
       // FMA-pipe polynomial for the power, packed FADD for the row sum.
-      if (UA_FWD_PINGPONG) named_bar_sync(bar_mine, 256);
       const float2 c2 = make_float2(c, c), nm2 = make_float2(-m_use, -m_use);
       float2 ls[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-      if (C::kSeparateP && j > 0) {  // P_t buffer free: PV_t(j-1) has consumed it
+      constexpr bool kLateP = C::kSeparateP && UA_FWD_LATEP && !UA_FWD_RELOAD;
+      if (C::kSeparateP && !kLateP && j > 0) {  // P_t buffer free: PV_t(j-1) has consumed it
         mbar_wait(&o_done[t], (j - 1) & 1);
         tc_fence_after();
       }
+      if (UA_FWD_PINGPONG) named_bar_sync(bar_mine, 256);
+      if (row == 0) UA_TEV(2 + t, j, 5);
 #if UA_FWD_RELOAD
       // software-pipelined: chunk k+1 is loaded from TMEM while chunk k is exponentiated
       uint32_t ra[32], rb[32];
@@ -380,6 +408,28 @@ __global__ void __launch_bounds__(384, 1) attn_fwd_kernel(const __grid_constant_
         mbar_arrive(&s_free[t]);
       }
 #else
+      if constexpr (kLateP) {
+        // All 128 exponentials into registers (64 packed words) first, so the
+        // wait for PV_t(j-1) to release the P buffer hides under them.
+        uint32_t pk[64];
+#pragma unroll
+        for (int cc = 0; cc < 128; cc += 32) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const float2 x = __ffma2_rn(make_float2(sv[cc + 2 * i], sv[cc + 2 * i + 1]), c2, nm2);
+            const bool poly = C::kPolyExp && poly_pair(i);
+            const float2 pp = poly ? exp2_poly2(x) : make_float2(ex2(x.x), ex2(x.y));
+            ls[i & 1] = __fadd2_rn(ls[i & 1], pp);
+            pk[cc / 2 + i] = pack_bf16x2(pp.x, pp.y);
+          }
+        }
+        if (j > 0) {
+          mbar_wait(&o_done[t], (j - 1) & 1);
+          tc_fence_after();
+        }
+#pragma unroll
+        for (int cc = 0; cc < 64; cc += 16) tmem_st16(t_lane + colP + cc, pk + cc);
+      } else {
 #pragma unroll
       for (int cc = 0; cc < 128; cc += 32) {
         uint32_t pk[16];
@@ -393,6 +443,7 @@ __global__ void __launch_bounds__(384, 1) attn_fwd_kernel(const __grid_constant_
           pk[i] = pack_bf16x2(pp.x, pp.y);
         }
         tmem_st16(t_lane + colP + cc / 2, pk);
+      }
       }
 #endif
       l += (ls[0].x + ls[0].y) + (ls[1].x + ls[1].y);
@@ -411,11 +462,11 @@ __global__ void __launch_bounds__(384, 1) attn_fwd_kernel(const __grid_constant_
           tmem_st32(t_lane + colO + cc, r);
         }
       }
-      if (row == 0) UA_TEV(2 + t, j, 5);
+      if (row == 0) UA_TEV(2 + t, j, 6);
       tmem_st_wait();
       tc_fence_before();
       mbar_arrive(&p_full[t]);
-      if (row == 0) UA_TEV(2 + t, j, 6);
+      if (row == 0) UA_TEV(2 + t, j, 7);
     }
 
     if (UA_FWD_PINGPONG && t == 0) named_bar_sync(1, 256);  // consume tile 1's last hand-back
@@ -458,6 +509,8 @@ __global__ void __launch_bounds__(384, 1) attn_fwd_kernel(const __grid_constant_
       }
     }
     if (valid) p.lse[b * p.l_sb + h * p.l_sh + q_row] = (m_use + __log2f(l)) * kLn2;
+  } else {
+    UA_FWD_REGS_LOW();  // warps 2, 3: idle members of the producer / MMA warpgroup
   }
 
   tc_fence_before();
