@@ -170,6 +170,31 @@ ua_status ua_lse_merge(float* o_a, float* lse_a, const float* o_b, const float* 
 /* fp32 [B][Hx][N][D] -> bf16 [B][N][Hx][D] (final cast of a merged result). */
 ua_status ua_f32_to_bf16_bnhd(const float* src, void* dst, int64_t B, int64_t N, int Hx, int D, ua_stream_t stream);
 
+/* ------------------------------------------------------------- LSS sequence parallelism
+ * The paper's other sequence-parallel strategy, Long Sequence Segmentation
+ * (§1, §2.5: "sequences are divided into segments, with
+ * each GPU computing a partial self-attention for its segment"; P:317, P:399:
+ * it has no head limit, unlike Ulysses).  Reading (Q16): rank r keeps
+ * its contiguous query segment of ALL H heads; K and V of every rank are
+ * gathered (one fused all-gather, 1 collective call); each rank computes exact
+ * attention of its N/P queries over all N keys.  Backward: dQ stays local; dK,
+ * dV partial sums over the local queries (fp32, all N keys) are summed over
+ * ranks and scattered to the key owners (one fused reduce-scatter).  Per call
+ * law: 1 collective in the forward, 2 in the backward (all-gather K/V again +
+ * reduce-scatter); 0 at P = 1, where both reduce to plain attention.
+ *   q, k, v, out, dout, dq, dk, dv : bf16 [B][N/P][H][D] (sequence shard)
+ *   lse : fp32 [B][H][N/P]   (this rank's queries, all heads)
+ * Constraints: N % P == 0, D in {32, 64, 128}; any H >= 1 and any P (P > H is
+ * allowed).  Same ownership / async / collective conventions as above.
+ * Collective calls and bytes are counted in ua_ctx_comm_stats. */
+ua_status ua_lss_validate(int64_t B, int64_t N, int H, int D, int P);
+ua_status ua_lss_workspace_size(int64_t B, int64_t N, int H, int D, int P, size_t* fwd_bytes, size_t* bwd_bytes);
+ua_status ua_lss_attn_fwd(ua_ctx* ctx, const void* q, const void* k, const void* v, void* out, float* lse, int64_t B,
+                          int64_t N, int H, int D, int P, void* workspace, size_t workspace_bytes, ua_stream_t stream);
+ua_status ua_lss_attn_bwd(ua_ctx* ctx, const void* q, const void* k, const void* v, const void* out, const float* lse,
+                          const void* dout, void* dq, void* dk, void* dv, int64_t B, int64_t N, int H, int D, int P,
+                          void* workspace, size_t workspace_bytes, ua_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

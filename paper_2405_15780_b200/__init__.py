@@ -30,7 +30,7 @@ EXPORTS = ("ua_version", "ua_status_string", "ua_last_error", "ua_validate", "ua
            "ua_get_unique_id", "ua_ctx_create", "ua_ctx_destroy", "ua_ctx_comm_stats",
            "ua_ctx_enable_timing", "ua_ctx_phase_times", "ua_ctx_set_a2a_mode", "ua_ctx_get_a2a_mode",
            "ua_ulysses_attn_fwd", "ua_ulysses_attn_bwd", "ua_attn_fwd_segment", "ua_lse_merge",
-           "ua_f32_to_bf16_bnhd")
+           "ua_f32_to_bf16_bnhd", "ua_lss_validate", "ua_lss_workspace_size", "ua_lss_attn_fwd", "ua_lss_attn_bwd")
 
 PHASES = ("pack_fwd", "a2a_fwd_in", "attn_fwd", "a2a_fwd_out", "unpack_fwd", "pack_bwd", "a2a_bwd_in",
           "attn_bwd", "dq_finalize", "a2a_bwd_out", "unpack_bwd")
@@ -78,6 +78,10 @@ def lib():
         L.ua_ctx_phase_times.argtypes = [vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i64)]
         L.ua_ulysses_attn_fwd.argtypes = [vp, vp, vp, vp, vp, vp, i64, i64, i32, i32, i32, vp, sz, vp]
         L.ua_ulysses_attn_bwd.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, i64, i64, i32, i32, i32, vp, sz, vp]
+        L.ua_lss_validate.argtypes = [i64, i64, i32, i32, i32]
+        L.ua_lss_workspace_size.argtypes = [i64, i64, i32, i32, i32, ctypes.POINTER(sz), ctypes.POINTER(sz)]
+        L.ua_lss_attn_fwd.argtypes = [vp, vp, vp, vp, vp, vp, i64, i64, i32, i32, i32, vp, sz, vp]
+        L.ua_lss_attn_bwd.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, i64, i64, i32, i32, i32, vp, sz, vp]
         L.ua_attn_fwd_segment.argtypes = [vp, vp, vp, vp, vp, i64, i64, i32, i32, i64, i64, vp]
         L.ua_lse_merge.argtypes = [vp, vp, vp, vp, i64, i32, vp]
         L.ua_f32_to_bf16_bnhd.argtypes = [vp, vp, i64, i64, i32, i32, vp]
@@ -243,6 +247,51 @@ def ulysses_attn_bwd(ctx: Context, q, k, v, out, lse, dout, dq=None, dk=None, dv
     _check(lib().ua_ulysses_attn_bwd(ctx.handle, _ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(lse), _ptr(dout),
                                      _ptr(dq), _ptr(dk), _ptr(dv), B, N, H, D, P, _ptr(ws), ws.numel(),
                                      _stream(stream)))
+    return dq, dk, dv
+
+
+def lss_validate(B: int, N: int, H: int, D: int, P: int) -> None:
+    """Host-only shape check of the LSS strategy (no head limit)."""
+    _check(lib().ua_lss_validate(B, N, H, D, P))
+
+
+def lss_workspace_size(B: int, N: int, H: int, D: int, P: int) -> tuple[int, int]:
+    f, b = ctypes.c_size_t(0), ctypes.c_size_t(0)
+    _check(lib().ua_lss_workspace_size(B, N, H, D, P, ctypes.byref(f), ctypes.byref(b)))
+    return f.value, b.value
+
+
+def lss_attn_fwd(ctx: Context, q, k, v, out=None, lse=None, stream=None) -> FwdOut:
+    """LSS sequence parallelism: q, k, v bf16 [B][N/P][H][D]
+    (this rank's segment).  Returns out [B][N/P][H][D] bf16 and lse [B][H][N/P] fp32."""
+    _need_cuda_bf16(q, k, v)
+    B, Nl, H, D = q.shape
+    P = ctx.P
+    N = Nl * P
+    out = torch.empty_like(q) if out is None else out
+    lse = torch.empty((B, H, Nl), dtype=torch.float32, device=q.device) if lse is None else lse
+    lss_validate(B, N, H, D, P)
+    fb, _ = lss_workspace_size(B, N, H, D, P)
+    ws = ctx.workspace(fb)
+    _check(lib().ua_lss_attn_fwd(ctx.handle, _ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(lse), B, N, H, D, P,
+                                 _ptr(ws), ws.numel(), _stream(stream)))
+    return FwdOut(out, lse)
+
+
+def lss_attn_bwd(ctx: Context, q, k, v, out, lse, dout, dq=None, dk=None, dv=None, stream=None):
+    """LSS backward: gradients (dq, dk, dv) bf16 [B][N/P][H][D] of this rank's segment."""
+    _need_cuda_bf16(q, k, v, out, dout)
+    B, Nl, H, D = q.shape
+    P = ctx.P
+    N = Nl * P
+    dq = torch.empty_like(q) if dq is None else dq
+    dk = torch.empty_like(k) if dk is None else dk
+    dv = torch.empty_like(v) if dv is None else dv
+    lss_validate(B, N, H, D, P)
+    _, bb = lss_workspace_size(B, N, H, D, P)
+    ws = ctx.workspace(bb)
+    _check(lib().ua_lss_attn_bwd(ctx.handle, _ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(lse), _ptr(dout), _ptr(dq),
+                                 _ptr(dk), _ptr(dv), B, N, H, D, P, _ptr(ws), ws.numel(), _stream(stream)))
     return dq, dk, dv
 
 

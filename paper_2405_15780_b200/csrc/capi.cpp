@@ -10,6 +10,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <initializer_list>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -202,6 +203,28 @@ BwdPlan plan_bwd(const Shape& s) {
   return p;
 }
 
+// LSS plans (P > 1).  KV gathered layout [N][B][H][D] (rank p's tokens at rows p*Nl..).
+struct LssPlan {
+  size_t kv_send = 0, kv_full = 0, delta = 0, dq_acc = 0, lsed = 0, part = 0, red = 0, total = 0;
+};
+LssPlan plan_lss(const Shape& s, bool bwd) {
+  LssPlan p;
+  if (s.P == 1) return p;
+  const size_t S = size_t(s.shard()) * 2;          // one bf16 [B][Nl][H][D] shard
+  p.kv_send = 0;                                    // [2][Nl][B][H][D] bf16 (B > 1: local K, V re-laid)
+  p.kv_full = align_up(p.kv_send + 2 * S);          // [2][N][B][H][D] bf16
+  p.total = align_up(p.kv_full + 2 * S * s.P);
+  if (!bwd) return p;
+  const int64_t n_pad = (s.Nl + 127) / 128 * 128;
+  p.delta = p.total;                                // [Nl][B][H] fp32
+  p.dq_acc = align_up(p.delta + size_t(s.B * s.Nl * s.H) * 4);         // [B*H][Nl_pad][D] fp32
+  p.lsed = align_up(p.dq_acc + size_t(s.B * s.H * n_pad * s.D) * 4);   // [B*H][Nl_pad] float2
+  p.part = align_up(p.lsed + size_t(s.B * s.H * n_pad) * 8);           // [2][N][B][H][D] fp32 partial dK, dV
+  p.red = align_up(p.part + 2 * S * 2 * s.P);                          // [2][Nl][B][H][D] fp32 reduced
+  p.total = align_up(p.red + 2 * S * 2);
+  return p;
+}
+
 // Fused all-to-all of `nt` equally-shaped tensors: peer chunk i of tensor w is
 // `count` elements at send[w] + i*count (bytes elem_size).  One NCCL group =
 // one collective call in the S:274 sense.
@@ -236,22 +259,28 @@ ua_status check_async(ua_ctx* ctx) {
   return UA_OK;
 }
 
-ua_status launch_attention_fwd(const void* q, const void* k, const void* v, int64_t sn, int64_t sh, int64_t sb,
-                               ua::ViewArg o, float* o_f32, int64_t of_sn, int64_t of_sh, int64_t of_sb, float* lse,
-                               int64_t l_sh, int64_t l_sb, int64_t B, int64_t N, int heads, int D, int64_t kv_begin,
-                               int64_t kv_end, cudaStream_t stream, const ua::PeerOut* o_peer = nullptr) {
+// Rows of a bf16 [.][rows][heads][D] view: base + token / head / batch strides (elements).
+struct Rows {
+  const void* base;
+  int64_t sn, sh, sb, n;
+};
+
+ua_status launch_attention_fwd(Rows q, const void* k, const void* v, Rows kv, ua::ViewArg o, float* o_f32,
+                               int64_t of_sn, int64_t of_sh, int64_t of_sb, float* lse, int64_t l_sh, int64_t l_sb,
+                               int64_t B, int heads, int D, int64_t kv_begin, int64_t kv_end, cudaStream_t stream,
+                               const ua::PeerOut* o_peer = nullptr) {
   ua::FwdParams p;
   std::memset(&p, 0, sizeof(p));
-  UA_TRY(make_map(&p.tm_q, q, D, N, heads, B, sn, sh, sb));
-  UA_TRY(make_map(&p.tm_k, k, D, N, heads, B, sn, sh, sb));
-  UA_TRY(make_map(&p.tm_v, v, D, N, heads, B, sn, sh, sb));
+  UA_TRY(make_map(&p.tm_q, q.base, D, q.n, heads, B, q.sn, q.sh, q.sb));
+  UA_TRY(make_map(&p.tm_k, k, D, kv.n, heads, B, kv.sn, kv.sh, kv.sb));
+  UA_TRY(make_map(&p.tm_v, v, D, kv.n, heads, B, kv.sn, kv.sh, kv.sb));
   p.o = o;
   if (o_peer) p.o_peer = *o_peer;
   p.o_f32 = o_f32;
   p.of_sn = of_sn; p.of_sh = of_sh; p.of_sb = of_sb;
   p.lse = lse;
   p.l_sh = l_sh; p.l_sb = l_sb;
-  p.n_q = int(N);
+  p.n_q = int(q.n);
   p.kv_begin = int(kv_begin);
   p.kv_end = int(kv_end);
   p.scale_log2 = float(1.4426950408889634 / std::sqrt(double(D)));
@@ -259,42 +288,68 @@ ua_status launch_attention_fwd(const void* q, const void* k, const void* v, int6
   return UA_OK;
 }
 
-ua_status launch_attention_bwd(const void* q, const void* k, const void* v, const void* dout, int64_t sn, int64_t sh,
-                               int64_t sb, ua::ViewArg dk, ua::ViewArg dv, float* dq_acc, const float* lse,
-                               int64_t l_sh, int64_t l_sb, const float* delta, int64_t d_sn, int64_t d_sh,
-                               int64_t d_sb, int64_t B, int64_t N, int heads, int D, float2* lsed,
-                               cudaStream_t stream, const ua::PeerOut* dk_peer = nullptr,
-                               const ua::PeerOut* dv_peer = nullptr) {
+// Square problem (queries and keys share N and strides).
+ua_status launch_attention_fwd(const void* q, const void* k, const void* v, int64_t sn, int64_t sh, int64_t sb,
+                               ua::ViewArg o, float* o_f32, int64_t of_sn, int64_t of_sh, int64_t of_sb, float* lse,
+                               int64_t l_sh, int64_t l_sb, int64_t B, int64_t N, int heads, int D, int64_t kv_begin,
+                               int64_t kv_end, cudaStream_t stream, const ua::PeerOut* o_peer = nullptr) {
+  const Rows r{q, sn, sh, sb, N};
+  return launch_attention_fwd(r, k, v, r, o, o_f32, of_sn, of_sh, of_sb, lse, l_sh, l_sb, B, heads, D, kv_begin,
+                              kv_end, stream, o_peer);
+}
+
+// Backward over queries q.n (q, dout share q's strides) and keys kv.n (k, v).
+// kv_f32: dk / dv views are fp32 partial sums.
+ua_status launch_attention_bwd(Rows q, const void* dout, const void* k, const void* v, Rows kv, ua::ViewArg dk,
+                               ua::ViewArg dv, int kv_f32, float* dq_acc, const float* lse, int64_t l_sh,
+                               int64_t l_sb, const float* delta, int64_t d_sn, int64_t d_sh, int64_t d_sb, int64_t B,
+                               int heads, int D, float2* lsed, cudaStream_t stream,
+                               const ua::PeerOut* dk_peer = nullptr, const ua::PeerOut* dv_peer = nullptr) {
   ua::BwdParams p;
   std::memset(&p, 0, sizeof(p));
   if (dk_peer) p.dk_peer = *dk_peer;
   if (dv_peer) p.dv_peer = *dv_peer;
+  const int64_t N = q.n;
   // (-lse*log2e, Delta) per query row, contiguous per head (bulk-loaded by the kernel)
   UA_CUDA(ua::launch_bwd_prep(lse, l_sh, l_sb, delta, d_sn, d_sh, d_sb, lsed, B, heads, N, stream));
   p.lsed = lsed;
-  UA_TRY(make_map(&p.tm_q, q, D, N, heads, B, sn, sh, sb));
-  UA_TRY(make_map(&p.tm_k, k, D, N, heads, B, sn, sh, sb));
-  UA_TRY(make_map(&p.tm_v, v, D, N, heads, B, sn, sh, sb));
-  UA_TRY(make_map(&p.tm_do, dout, D, N, heads, B, sn, sh, sb));
-  UA_TRY(make_map(&p.tm_qh, q, D, N, heads, B, sn, sh, sb, 64));
-  UA_TRY(make_map(&p.tm_doh, dout, D, N, heads, B, sn, sh, sb, 64));
+  UA_TRY(make_map(&p.tm_q, q.base, D, N, heads, B, q.sn, q.sh, q.sb));
+  UA_TRY(make_map(&p.tm_do, dout, D, N, heads, B, q.sn, q.sh, q.sb));
+  UA_TRY(make_map(&p.tm_qh, q.base, D, N, heads, B, q.sn, q.sh, q.sb, 64));
+  UA_TRY(make_map(&p.tm_doh, dout, D, N, heads, B, q.sn, q.sh, q.sb, 64));
+  UA_TRY(make_map(&p.tm_k, k, D, kv.n, heads, B, kv.sn, kv.sh, kv.sb));
+  UA_TRY(make_map(&p.tm_v, v, D, kv.n, heads, B, kv.sn, kv.sh, kv.sb));
   const int64_t n_pad = (N + 127) / 128 * 128;
   if (!ua::make_tmap_f32_2d(&p.tm_dq, dq_acc, uint64_t(D), uint64_t(B * heads * n_pad), 128))
     return fail(UA_ERR_CUDA, "cuTensorMapEncodeTiled failed for dq_acc");
   p.dk = dk;
   p.dv = dv;
+  p.kv_f32 = kv_f32;
   p.dq_acc = dq_acc;
   p.lse = lse;
   p.l_sh = l_sh; p.l_sb = l_sb;
   p.delta = delta;
   p.d_sn = d_sn; p.d_sh = d_sh; p.d_sb = d_sb;
   p.n = int(N);
+  p.n_kv = int(kv.n);
   p.heads = heads;
   p.batch = int(B);
   p.scale = float(1.0 / std::sqrt(double(D)));
   p.scale_log2 = float(1.4426950408889634 / std::sqrt(double(D)));
   UA_CUDA(ua::launch_attn_bwd(p, D, int(B), heads, stream));
   return UA_OK;
+}
+
+// Square problem.
+ua_status launch_attention_bwd(const void* q, const void* k, const void* v, const void* dout, int64_t sn, int64_t sh,
+                               int64_t sb, ua::ViewArg dk, ua::ViewArg dv, float* dq_acc, const float* lse,
+                               int64_t l_sh, int64_t l_sb, const float* delta, int64_t d_sn, int64_t d_sh,
+                               int64_t d_sb, int64_t B, int64_t N, int heads, int D, float2* lsed,
+                               cudaStream_t stream, const ua::PeerOut* dk_peer = nullptr,
+                               const ua::PeerOut* dv_peer = nullptr) {
+  const Rows r{q, sn, sh, sb, N};
+  return launch_attention_bwd(r, dout, k, v, r, dk, dv, 0, dq_acc, lse, l_sh, l_sb, delta, d_sn, d_sh, d_sb, B, heads,
+                              D, lsed, stream, dk_peer, dv_peer);
 }
 
 // ------------------------------------------------------------ peer all-to-all
@@ -747,6 +802,166 @@ ua_status ua_ulysses_attn_bwd(ua_ctx* ctx, const void* q, const void* k, const v
     const void* usrc[3] = {rgrad[0], rgrad[1], rgrad[2]};
     void* udst[3] = {dq, dk, dv};
     UA_CUDA(ua::launch_unpack(usrc, udst, 3, B, s.Nl, H, D, P, stream));
+  }
+  return UA_OK;
+}
+
+// ------------------------------------------------------------ LSS sequence parallelism
+ua_status ua_lss_validate(int64_t B, int64_t N, int H, int D, int P) {
+  if (B < 1 || N < 1 || H < 1 || D < 1 || P < 1)
+    return fail(UA_ERR_INVALID_ARG, "B, N, H, D, P must be >= 1 (got B=%lld N=%lld H=%d D=%d P=%d)", (long long)B,
+                (long long)N, H, D, P);
+  if (N % P != 0) return fail(UA_ERR_SEQ_DIVISIBILITY, "LSS needs N %% P == 0 (N=%lld, P=%d)", (long long)N, P);
+  if (D != 32 && D != 64 && D != 128) return fail(UA_ERR_UNSUPPORTED, "head dim D=%d not in {32, 64, 128}", D);
+  if (N >= (int64_t(1) << 31)) return fail(UA_ERR_UNSUPPORTED, "N=%lld >= 2^31", (long long)N);
+  if (B * N * H >= (int64_t(1) << 40)) return fail(UA_ERR_UNSUPPORTED, "problem too large");
+  return UA_OK;
+}
+
+ua_status ua_lss_workspace_size(int64_t B, int64_t N, int H, int D, int P, size_t* fwd_bytes, size_t* bwd_bytes) {
+  UA_TRY(ua_lss_validate(B, N, H, D, P));
+  const Shape s = make_shape(B, N, H, D, P);
+  if (P == 1) {  // plain attention on the whole sequence: the Ulysses P = 1 plan
+    if (fwd_bytes) *fwd_bytes = plan_fwd(s).total;
+    if (bwd_bytes) *bwd_bytes = plan_bwd(s).total;
+    return UA_OK;
+  }
+  if (fwd_bytes) *fwd_bytes = plan_lss(s, false).total;
+  if (bwd_bytes) *bwd_bytes = plan_lss(s, true).total;
+  return UA_OK;
+}
+
+namespace {
+// K, V of every rank into kv_full [2][N][B][H][D]: one fused all-gather (NCCL group of two).
+ua_status lss_gather_kv(ua_ctx* ctx, const Shape& s, const void* k, const void* v, char* ws, const LssPlan& plan,
+                        int ph_pack, int ph_gather, cudaStream_t stream) {
+  const size_t S = size_t(s.shard()) * 2;
+  const void* kv_src[2] = {k, v};
+  void* kv_send[2] = {ws + plan.kv_send, ws + plan.kv_send + S};
+  if (s.B > 1) {  // [B][Nl][H][D] -> [Nl][B][H][D] (pack with one destination)
+    Phase ph(ctx, ph_pack, stream);
+    UA_CUDA(ua::launch_pack(kv_src, kv_send, 2, s.B, s.Nl, s.H, s.D, 1, nullptr, nullptr, nullptr, stream));
+  } else {
+    kv_send[0] = const_cast<void*>(k);
+    kv_send[1] = const_cast<void*>(v);
+  }
+  Phase ph(ctx, ph_gather, stream);
+  UA_NCCL(ncclGroupStart());
+  for (int w = 0; w < 2; ++w) {
+    ncclResult_t r = ncclAllGather(kv_send[w], ws + plan.kv_full + size_t(w) * S * s.P, size_t(s.shard()),
+                                   ncclBfloat16, ctx->comm, stream);
+    if (r != ncclSuccess) {
+      ncclGroupEnd();
+      return fail(UA_ERR_NCCL, "ncclAllGather: %s", ncclGetErrorString(r));
+    }
+  }
+  UA_NCCL(ncclGroupEnd());
+  ctx->a2a_calls += 1;
+  ctx->a2a_bytes += int64_t(s.P - 1) * int64_t(S) * 2;
+  return UA_OK;
+}
+
+ua_status lss_check_call(ua_ctx* ctx, int64_t B, int64_t N, int H, int D, int P, std::initializer_list<const void*> ptrs,
+                         size_t need, void* workspace, size_t workspace_bytes) {
+  UA_TRY(ua_lss_validate(B, N, H, D, P));
+  if (!ctx) return fail(UA_ERR_INVALID_ARG, "ctx is NULL");
+  if (P != ctx->P) return fail(UA_ERR_INVALID_ARG, "P=%d differs from ctx P=%d", P, ctx->P);
+  for (const void* ptr : ptrs) {
+    if (!ptr) return fail(UA_ERR_INVALID_ARG, "null tensor pointer");
+    if (!aligned16(ptr)) return fail(UA_ERR_INVALID_ARG, "tensor pointers must be 16-byte aligned");
+  }
+  if (workspace_bytes < need || (need > 0 && !workspace))
+    return fail(UA_ERR_INVALID_ARG, "workspace too small: need %zu bytes, got %zu", need, workspace_bytes);
+  UA_TRY(check_device());
+  return check_async(ctx);
+}
+}  // namespace
+
+ua_status ua_lss_attn_fwd(ua_ctx* ctx, const void* q, const void* k, const void* v, void* out, float* lse, int64_t B,
+                          int64_t N, int H, int D, int P, void* workspace, size_t workspace_bytes, ua_stream_t stream_) {
+  cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
+  const Shape s = make_shape(B, N, H, D, P);
+  const LssPlan plan = plan_lss(s, false);
+  UA_TRY(lss_check_call(ctx, B, N, H, D, P, {q, k, v, out, lse}, plan.total, workspace, workspace_bytes));
+  if (P == 1) return ua_ulysses_attn_fwd(ctx, q, k, v, out, lse, B, N, H, D, 1, workspace, workspace_bytes, stream_);
+  char* ws = static_cast<char*>(workspace);
+  UA_TRY(lss_gather_kv(ctx, s, k, v, ws, plan, UA_PHASE_PACK_FWD, UA_PHASE_A2A_FWD_IN, stream));
+  // exact attention of the local query segment over all N keys, every head
+  const size_t S = size_t(s.shard()) * 2;
+  const int64_t qsn = int64_t(H) * D, qsh = D, qsb = s.Nl * H * D;
+  const Rows qr{q, qsn, qsh, qsb, s.Nl};
+  const Rows kvr{nullptr, B * int64_t(H) * D, D, int64_t(H) * D, N};
+  ua::ViewArg o{out, qsn, qsh, qsb};
+  Phase ph(ctx, UA_PHASE_ATTN_FWD, stream);
+  return launch_attention_fwd(qr, ws + plan.kv_full, ws + plan.kv_full + S * P, kvr, o, nullptr, 0, 0, 0, lse, s.Nl,
+                              int64_t(H) * s.Nl, B, H, D, 0, N, stream);
+}
+
+ua_status ua_lss_attn_bwd(ua_ctx* ctx, const void* q, const void* k, const void* v, const void* out, const float* lse,
+                          const void* dout, void* dq, void* dk, void* dv, int64_t B, int64_t N, int H, int D, int P,
+                          void* workspace, size_t workspace_bytes, ua_stream_t stream_) {
+  cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
+  const Shape s = make_shape(B, N, H, D, P);
+  const LssPlan plan = plan_lss(s, true);
+  UA_TRY(lss_check_call(ctx, B, N, H, D, P, {q, k, v, out, lse, dout, dq, dk, dv}, plan.total, workspace,
+                        workspace_bytes));
+  if (P == 1)
+    return ua_ulysses_attn_bwd(ctx, q, k, v, out, lse, dout, dq, dk, dv, B, N, H, D, 1, workspace, workspace_bytes,
+                               stream_);
+  char* ws = static_cast<char*>(workspace);
+  const size_t S = size_t(s.shard()) * 2;
+  const int64_t Nl = s.Nl;
+  const int64_t n_pad = (Nl + 127) / 128 * 128;
+  const float scale = float(1.0 / std::sqrt(double(D)));
+  UA_TRY(lss_gather_kv(ctx, s, k, v, ws, plan, UA_PHASE_PACK_BWD, UA_PHASE_A2A_BWD_IN, stream));
+  float* delta = reinterpret_cast<float*>(ws + plan.delta);
+  float* dq_acc = reinterpret_cast<float*>(ws + plan.dq_acc);
+  float* part = reinterpret_cast<float*>(ws + plan.part);
+  float* red = reinterpret_cast<float*>(ws + plan.red);
+  {  // Delta[t][b][h] = sum_d dO.O (fp32), local queries
+    Phase ph(ctx, UA_PHASE_PACK_BWD, stream);
+    UA_CUDA(ua::launch_pack(nullptr, nullptr, 0, B, Nl, H, D, 1, dout, out, delta, stream));
+  }
+  const int64_t qsn = int64_t(H) * D, qsh = D, qsb = Nl * H * D;
+  const int64_t ksn = B * int64_t(H) * D, ksh = D, ksb = int64_t(H) * D;
+  const size_t PE = size_t(s.shard()) * s.P;  // elements of one [N][B][H][D] tensor
+  {  // local dQ; dK, dV partial sums over the local queries for all N keys (fp32)
+    Phase ph(ctx, UA_PHASE_ATTN_BWD, stream);
+    UA_CUDA(cudaMemsetAsync(dq_acc, 0, size_t(B * H * n_pad * D) * 4, stream));
+    const Rows qr{q, qsn, qsh, qsb, Nl};
+    const Rows kvr{nullptr, ksn, ksh, ksb, N};
+    ua::ViewArg vdk{part, ksn, ksh, ksb}, vdv{part + PE, ksn, ksh, ksb};
+    UA_TRY(launch_attention_bwd(qr, dout, ws + plan.kv_full, ws + plan.kv_full + S * P, kvr, vdk, vdv, 1, dq_acc, lse,
+                                Nl, int64_t(H) * Nl, delta, B * int64_t(H), 1, H, B, H, D,
+                                reinterpret_cast<float2*>(ws + plan.lsed), stream));
+  }
+  {
+    Phase ph(ctx, UA_PHASE_DQ_FINALIZE, stream);
+    ua::ViewArg vdq{dq, qsn, qsh, qsb};
+    UA_CUDA(ua::launch_dq_finalize(dq_acc, vdq, B, Nl, H, D, scale, stream));
+  }
+  {  // dK, dV partials summed over ranks into the key owners (one fused reduce-scatter)
+    Phase ph(ctx, UA_PHASE_A2A_BWD_OUT, stream);
+    UA_NCCL(ncclGroupStart());
+    for (int w = 0; w < 2; ++w) {
+      ncclResult_t r = ncclReduceScatter(part + w * PE, red + w * size_t(s.shard()), size_t(s.shard()), ncclFloat32,
+                                         ncclSum, ctx->comm, stream);
+      if (r != ncclSuccess) {
+        ncclGroupEnd();
+        return fail(UA_ERR_NCCL, "ncclReduceScatter: %s", ncclGetErrorString(r));
+      }
+    }
+    UA_NCCL(ncclGroupEnd());
+    ctx->a2a_calls += 1;
+    ctx->a2a_bytes += int64_t(s.P - 1) * int64_t(s.shard()) * 4 * 2;
+  }
+  {  // [Nl][B][H][D] fp32 -> bf16 [B][Nl][H][D]
+    Phase ph(ctx, UA_PHASE_UNPACK_BWD, stream);
+    void* dsts[2] = {dk, dv};
+    for (int w = 0; w < 2; ++w) {
+      ua::ViewArg vo{dsts[w], D, Nl * H * D, int64_t(H) * D};
+      UA_CUDA(ua::launch_f32_to_view(red + w * size_t(s.shard()), vo, Nl, H, int(B), D, stream));
+    }
   }
   return UA_OK;
 }

@@ -40,9 +40,18 @@
 #define UA_BWD_STAGGER 16   // query-tile window the persistent CTAs' start tiles are spread over
 #endif
 
+#ifndef UA_BWD_DQ_RED
+#define UA_BWD_DQ_RED 0     // dQ drain: 1 = red.global.add.v4.f32 from registers, 0 = smem box + TMA reduce-add
+#endif
+
 namespace ua {
 
 namespace {
+
+__device__ __forceinline__ void red_add_f32x4(float* addr, float a, float b, float c, float d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b), "f"(c), "f"(d)
+               : "memory");
+}
 
 template <int D>
 struct BwdWsCfg {
@@ -102,7 +111,7 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_ws_kernel(const __grid_consta
   const int lane = threadIdx.x % 32;
   const int n_q = (p.n + 127) / 128;
   const int n_pad = n_q * 128;
-  const int n_kt = n_q;
+  const int n_kt = (p.n_kv + 127) / 128;
   const int n_items = p.batch * p.heads * n_kt;
   const int start = int((int64_t(blockIdx.x) * C::kStagger) / gridDim.x) % n_q;
   auto qslot = [&](int s) { return sSlots + s * C::kSlotBytes; };
@@ -386,7 +395,7 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_ws_kernel(const __grid_consta
       mbar_wait(acc_full, it & 1);
       tc_fence_after();
       const int krow = kt * 128 + j;
-      const bool valid = krow < p.n;
+      const bool valid = krow < p.n_kv;
       const ViewArg& dst_v = hh == 0 ? p.dv : p.dk;
       const uint32_t col = hh == 0 ? C::kColDV : C::kColDK;
       const float sc = hh == 0 ? 1.f : p.scale;
@@ -397,6 +406,22 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_ws_kernel(const __grid_consta
         const int owner = int(krow / po.nl);
         dst = reinterpret_cast<__nv_bfloat16*>(po.base[owner]) + ((b * po.nl + (krow - owner * po.nl)) * po.H + po.h0 + h) * D;
       }
+      if (p.kv_f32) {  // fp32 partial sums (LSS: reduce-scattered across ranks afterwards)
+        float* fdst = reinterpret_cast<float*>(dst_v.base) + b * dst_v.sb + h * dst_v.sh + int64_t(krow) * dst_v.sn;
+#pragma unroll
+        for (int cc = 0; cc < D; cc += 16) {
+          uint32_t r[16];
+          tmem_ld16(t_lane + col + cc, r);
+          tmem_ld_wait();
+          if (valid) {
+#pragma unroll
+            for (int x = 0; x < 16; x += 4)
+              *reinterpret_cast<float4*>(fdst + cc + x) =
+                  make_float4(__uint_as_float(r[x]) * sc, __uint_as_float(r[x + 1]) * sc,
+                              __uint_as_float(r[x + 2]) * sc, __uint_as_float(r[x + 3]) * sc);
+          }
+        }
+      } else
 #pragma unroll
       for (int cc = 0; cc < D; cc += 16) {
         uint32_t r[16];
@@ -446,6 +471,14 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_ws_kernel(const __grid_consta
             mbar_arrive(dq_empty);
             if (r == 0) UA_TEV(4, T, 3);
           }
+#if UA_BWD_DQ_RED
+          {  // straight from registers: fp32 vector reductions into dq_acc (no smem staging)
+            float* dst = p.dq_acc + (int64_t(bh) * n_pad + tile * 128 + r) * D + rd * kCols;
+#pragma unroll
+            for (int e = 0; e < kCols; e += 4) red_add_f32x4(dst + e, acc[e], acc[e + 1], acc[e + 2], acc[e + 3]);
+          }
+          if (false)
+#endif
           // kCols / 32 boxes through kStageBoxes staging boxes
 #pragma unroll
           for (int cb0 = 0; cb0 < kCols / 32; cb0 += C::kStageBoxes) {
@@ -493,7 +526,7 @@ cudaError_t launch_bwd_ws_impl(const BwdParams& p, cudaStream_t stream) {
         cudaFuncSetAttribute(attn_bwd_ws_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
     if (e != cudaSuccess) return e;
   }
-  const int64_t items = int64_t(p.batch) * p.heads * ((p.n + 127) / 128);
+  const int64_t items = int64_t(p.batch) * p.heads * ((p.n_kv + 127) / 128);
   const int grid = int(items < num_sms ? items : num_sms);
 #if UA_TRACE
   trace_reset();

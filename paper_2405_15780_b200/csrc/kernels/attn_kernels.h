@@ -66,7 +66,9 @@ struct alignas(64) BwdParams {
   const float* delta; // Delta[b*d_sb + h*d_sh + n*d_sn]
   int64_t d_sn, d_sh, d_sb;
   const float2* lsed; // per head, per 128-row tile: [128 x -lse*log2(e)][128 x -Delta]; rows >= N: (-inf, 0)
-  int n;              // sequence length (queries == keys)
+  int n;              // number of queries (rows of Q, dO, lse, Delta, dq_acc)
+  int n_kv;           // number of keys (rows of K, V, dK, dV); == n except for LSS (local queries, all keys)
+  int kv_f32;         // 1: dk / dv views are fp32 (unrounded partial sums, LSS reduce-scatter input)
   int heads;
   int batch;
   float scale;        // 1/sqrt(D)

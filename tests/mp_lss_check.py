@@ -1,0 +1,102 @@
+"""Multi-rank LSS (Long Sequence Segmentation) parity check, launched by
+tests/test_multigpu.py as
+    torchrun --nproc-per-node P tests/mp_lss_check.py --N .. --H .. --D .. [--B ..]
+Each rank feeds its contiguous sequence segment (sliced from the same synth
+global tensors) through ua_lss_attn_fwd / _bwd with P ranks (PAPER.md P:72,
+P:166; Q16); rank 0 gathers and checks:
+  * P-way forward == P=1 forward, bitwise (each query row sees the same key
+    tiles in the same order);
+  * out / lse / dq / dk / dv against the fp64 dense oracle (tests/parity.py);
+  * the collective law: 1 call in the forward (all-gather K, V), 2 in the
+    backward (all-gather K, V; reduce-scatter dK, dV) and their byte counts;
+  * P > H runs (no head limit).
+Prints "LSS_OK" on success."""
+import argparse
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import oracle  # noqa: E402
+import paper_2405_15780_b200 as ua  # noqa: E402
+import synth  # noqa: E402
+from tests.parity import gate_grad, gate_lse, gate_out  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--B", type=int, default=1)
+    ap.add_argument("--N", type=int, default=4096)
+    ap.add_argument("--H", type=int, default=8)
+    ap.add_argument("--D", type=int, default=64)
+    ap.add_argument("--sigma", type=float, default=1.0)
+    a = ap.parse_args()
+    rank, P = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    B, N, H, D = a.B, a.N, a.H, a.D
+    Nl = N // P
+    q, k, v, do = synth.qkv(B, N, H, D, seed=91, sigma_qk=a.sigma, with_do=True)
+    sl = slice(rank * Nl, (rank + 1) * Nl)
+    qs, ks, vs, ds = (t[:, sl].contiguous().to(dev) for t in (q, k, v, do))
+
+    ctx = ua.Context(P=P, rank=rank, device=local)
+    c0, b0 = ctx.comm_stats()
+    r = ua.lss_attn_fwd(ctx, qs, ks, vs)
+    c1, b1 = ctx.comm_stats()
+    dq, dk, dv = ua.lss_attn_bwd(ctx, qs, ks, vs, r.out, r.lse, ds)
+    c2, b2 = ctx.comm_stats()
+    torch.cuda.synchronize()
+    assert (c1 - c0, c2 - c1) == (1, 2), (c0, c1, c2)
+    S = B * Nl * H * D                                   # elements of one shard
+    assert b1 - b0 == (P - 1) * S * 2 * 2, (b1 - b0)    # K, V bf16 from P-1 peers
+    assert b2 - b1 == (P - 1) * S * 2 * 2 + (P - 1) * S * 4 * 2, (b2 - b1)  # + fp32 dK, dV partials
+    assert r.lse.shape == (B, H, Nl)
+    # a second step: same bits for the forward and for dk / dv (deterministic reduce-scatter)
+    r2 = ua.lss_attn_fwd(ctx, qs, ks, vs)
+    dq2, dk2, dv2 = ua.lss_attn_bwd(ctx, qs, ks, vs, r2.out, r2.lse, ds)
+    torch.cuda.synchronize()
+    assert torch.equal(r2.out, r.out) and torch.equal(r2.lse, r.lse)
+    assert torch.equal(dk2, dk) and torch.equal(dv2, dv)
+
+    def gather(t):
+        parts = [torch.empty_like(t) for _ in range(P)]
+        dist.all_gather(parts, t.contiguous())
+        return parts
+
+    outs, dqs, dks, dvs, lses = (gather(t) for t in (r.out, dq, dk, dv, r.lse))
+    if rank == 0:
+        out_g = torch.cat(outs, 1).float().cpu().numpy()
+        lse_g = torch.cat(lses, 2).cpu().numpy()            # [B][H][N]: rank j holds queries block j
+        dq_g, dk_g, dv_g = (torch.cat(x, 1).float().cpu().numpy() for x in (dqs, dks, dvs))
+        c1ctx = ua.Context(P=1, device=local)
+        r1 = ua.lss_attn_fwd(c1ctx, q.to(dev), k.to(dev), v.to(dev))
+        g1 = ua.lss_attn_bwd(c1ctx, q.to(dev), k.to(dev), v.to(dev), r1.out, r1.lse, do.to(dev))
+        torch.cuda.synchronize()
+        assert np.array_equal(out_g, r1.out.float().cpu().numpy()), "P-way LSS forward != P=1 forward"
+        assert np.array_equal(lse_g, r1.lse.cpu().numpy()), "P-way LSS lse != P=1 lse"
+        for x, y in zip((dq_g, dk_g, dv_g), g1):
+            assert np.abs(x - y.float().cpu().numpy()).max() <= 2e-2
+        f64 = [synth.to_f64(t) for t in (q, k, v, do)]
+        ref, ref_lse, absv = oracle.attn_fwd(*f64[:3], with_abs=True)
+        gate_out(out_g, ref, gate_a=a.sigma == 1.0, absv=absv)
+        gate_lse(lse_g, ref_lse)
+        rdq, rdk, rdv, _, _, gabs = oracle.attn_bwd(*f64, with_abs=True)
+        for x, y, gb in zip((dq_g, dk_g, dv_g), (rdq, rdk, rdv), gabs):
+            gate_grad(x, y, gate_a=a.sigma == 1.0, gabs=gb)
+        c1ctx.close()
+        print("LSS_OK", flush=True)
+    ctx.close()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -95,3 +95,33 @@ def test_no_cpu_fallback():
     assert st in (4, 5)
     with pytest.raises(ValueError):
         ua.ulysses_attn_fwd(None, torch.zeros(1, 4, 1, 64), torch.zeros(1, 4, 1, 64), torch.zeros(1, 4, 1, 64))
+
+
+@pytest.mark.parametrize("args,status", [
+    ((1, 16, 4, 64, 8), 0),       # LSS has no head limit: H=4, P=8 is fine
+    ((1, 12, 6, 64, 4), 0),       # P need not divide H
+    ((1, 10, 4, 64, 4), 3),       # N % P != 0 -> SeqDivisibility
+    ((1, 16, 4, 72, 2), 4),
+    ((0, 16, 4, 64, 1), 1),
+    ((1, 188416, 32, 64, 8), 0),
+    ((1, 1048576, 32, 128, 64), 0),
+])
+def test_lss_validate_codes(args, status):
+    assert ua.lib().ua_lss_validate(*args) == status
+
+
+def test_lss_workspace_plan():
+    """LSS forward gathers K, V ([2][N][B][H][D] bf16 + local send copy); the
+    backward adds fp32 partial dK, dV for all N keys and their reduced shard."""
+    B, N, H, D = 1, 188416, 32, 64
+    full = B * N * H * D
+    assert ua.lss_workspace_size(B, N, H, D, 1) == ua.workspace_size(B, N, H, D, 1)
+    for P in (2, 4, 8):
+        f, b = ua.lss_workspace_size(B, N, H, D, P)
+        s = full // P
+        assert 2 * 2 * full + 2 * 2 * s <= f <= 2 * 2 * full + 2 * 2 * s + 4096
+        assert b >= f + 2 * 4 * full + 2 * 4 * s + (N // P) * H * 4
+    # P > H works for LSS, not for Ulysses
+    assert ua.lss_workspace_size(1, 4096, 2, 64, 4)[0] > 0
+    with pytest.raises(ua.HeadDivisibilityError):
+        ua.workspace_size(1, 4096, 2, 64, 4)

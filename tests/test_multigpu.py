@@ -39,6 +39,24 @@ def test_ulysses_p_way(P, N, H, D, sigma, mode):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("P,B,N,H,D,sigma", [
+    (2, 1, 4096, 8, 64, 1.0),
+    (2, 1, 2048, 4, 128, 2.0),
+    (2, 1, 4050, 4, 64, 1.0),     # ragged segment: N/P = 2025
+    (2, 2, 2048, 4, 64, 1.0),     # B > 1: K, V re-laid [Nl][B][H][D] before the gather
+    (4, 1, 4096, 2, 64, 1.0),     # P > H: no head limit
+    (4, 1, 4096, 8, 32, 2.0),
+    (8, 1, 8192, 4, 64, 1.0),
+])
+def test_lss_p_way(P, B, N, H, D, sigma):
+    if torch.cuda.device_count() < P:
+        pytest.skip(f"needs {P} GPUs")
+    r = torchrun(P, os.path.join(ROOT, "tests", "mp_lss_check.py"), f"--B={B}", f"--N={N}", f"--H={H}", f"--D={D}",
+                 f"--sigma={sigma}")
+    assert r.returncode == 0 and "LSS_OK" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
+
+
+@pytest.mark.gpu
 @pytest.mark.slow
 @pytest.mark.parametrize("config,P,mode", [("c3", 1, "nccl"), ("c4", 1, "nccl"),
                                            ("c3", 2, "nccl"), ("c3", 4, "nccl"), ("c3", 8, "nccl"),
@@ -69,6 +87,11 @@ codes = [ua.lib().ua_validate(1, 16, 1, 64, P), ua.lib().ua_validate(1, 15, 4, 6
 allc = [None] * P
 dist.all_gather_object(allc, codes)
 assert all(c == [2, 3, 0] for c in allc), allc
+# 1b) LSS validation: no head limit (P:317), same codes on every rank
+lcodes = [ua.lib().ua_lss_validate(1, 16, 1, 64, P), ua.lib().ua_lss_validate(1, 15, 4, 64, P)]
+allc = [None] * P
+dist.all_gather_object(allc, lcodes)
+assert all(c == [0, 3] for c in allc), allc
 # 2) the oracle's all-to-all (S:122) equals torch.distributed.all_to_all (library routine)
 B, N, H, D = 1, 8, 4, 2
 x = np.arange(B * N * H * D, dtype=np.float64).reshape(B, N, H, D)
