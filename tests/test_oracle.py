@@ -298,6 +298,36 @@ def test_lss_merge_weights_are_segment_mass():
     assert np.abs(mass - 1).max() < 1e-14
 
 
+@pytest.mark.parametrize("P,B,N,H,D", [(1, 1, 24, 2, 8), (2, 1, 24, 2, 8), (3, 2, 27, 1, 4), (4, 1, 32, 3, 16),
+                                       (6, 1, 24, 2, 8)])
+def test_lss_sp_equals_dense(P, B, N, H, D):
+    """LSS sequence parallelism: per-rank forward over gathered keys and
+    the reduce-scattered partial dK, dV reproduce the dense fp64 oracle (the C
+    implementation, a different code path) -- including P > H."""
+    q, k, v, do = (rnd((B, N, H, D), s, 1.5) for s in (110, 111, 112, 113))
+    out, lse = oracle.attn_fwd(q, k, v)
+    dq, dk, dv, _, _ = oracle.attn_bwd(q, k, v, do)
+    outs, lses = lss.sp_fwd(q, k, v, P)
+    assert np.abs(np.concatenate(outs, 1) - out).max() < 1e-12
+    assert np.abs(np.concatenate(lses, 2) - lse).max() < 1e-12
+    dqs, dks, dvs = lss.sp_bwd(q, k, v, do, P)
+    for got, ref in ((dqs, dq), (dks, dk), (dvs, dv)):
+        assert np.abs(np.concatenate(got, 1) - ref).max() < 1e-11
+
+
+def test_lss_sp_partials_are_partial():
+    """A single rank's dK partial is NOT the full dK (P > 1) -- the reduce is
+    needed -- and the partials of the ranks sum to it."""
+    P, N, H, D = 2, 16, 1, 4
+    q, k, v, do = (rnd((1, N, H, D), s) for s in (120, 121, 122, 123))
+    _, dk, _, out, lse = oracle.attn_bwd(q, k, v, do)
+    Nl = N // P
+    parts = [lss.sp_bwd_partial(q[:, r * Nl:(r + 1) * Nl], do[:, r * Nl:(r + 1) * Nl], out[:, r * Nl:(r + 1) * Nl],
+                                lse[:, :, r * Nl:(r + 1) * Nl], k, v)[1] for r in range(P)]
+    assert np.abs(parts[0] - dk).max() > 1e-3
+    assert np.abs(parts[0] + parts[1] - dk).max() < 1e-12
+
+
 def test_bwd_abs_helpers():
     """gabs = (scale (|dS|+E)|K|, scale (|dS|+E)^T|Q|, P^T|dO|): the third equals dV
     computed with |dO| (dV is linear in dO); all bound |grad| from above; the
