@@ -180,6 +180,8 @@ def main():
     ap.add_argument("--a2a", default="nccl", choices=["nccl", "peer"],
                     help="all-to-all transport for P > 1: NCCL send/recv, or NVLink peer stores from the kernels")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--strategy", default="ulysses", choices=["ulysses", "lss"],
+                    help="sequence-parallel strategy: Ulysses all-to-all (headline) or LSS gather-KV / reduce-scatter")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -197,26 +199,29 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     B, N, H, D = WORKLOAD["B"], args.N, args.H, args.D
-    ua.validate(B, N, H, D, P)
+    lss = args.strategy == "lss"
+    (ua.lss_validate if lss else ua.validate)(B, N, H, D, P)
     Nl = N // P
+    fwd_fn = ua.lss_attn_fwd if lss else ua.ulysses_attn_fwd
+    bwd_fn = ua.lss_attn_bwd if lss else ua.ulysses_attn_bwd
     ctx = ua.Context(P=P, rank=rank, device=local)
-    if P > 1:
+    if P > 1 and not lss:
         ctx.set_a2a_mode(args.a2a)
     dev = torch.device("cuda", local)
     g = torch.Generator(device=dev).manual_seed(1234 + rank)
     shape = (B, Nl, H, D)
     q, k, v, do = (torch.randn(shape, device=dev, generator=g, dtype=torch.float32).to(torch.bfloat16)
                    for _ in range(4))
-    fb, bb = ua.workspace_size(B, N, H, D, P)
+    fb, bb = (ua.lss_workspace_size if lss else ua.workspace_size)(B, N, H, D, P)
     ctx.workspace(max(fb, bb))
     out = torch.empty_like(q)
-    lse = torch.empty((B, H // P, N), dtype=torch.float32, device=dev)
+    lse = torch.empty((B, H, Nl) if lss else (B, H // P, N), dtype=torch.float32, device=dev)
     dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
     stream = torch.cuda.current_stream()
 
     def step(qq=q, kk=k, vv=v, dd=do):
-        ua.ulysses_attn_fwd(ctx, qq, kk, vv, out=out, lse=lse)
-        ua.ulysses_attn_bwd(ctx, qq, kk, vv, out, lse, dd, dq=dq, dk=dk, dv=dv)
+        fwd_fn(ctx, qq, kk, vv, out=out, lse=lse)
+        bwd_fn(ctx, qq, kk, vv, out, lse, dd, dq=dq, dk=dk, dv=dv)
 
     def barrier():
         if dist is not None:
@@ -272,7 +277,7 @@ def main():
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp)).get(f"attn_bwd_D{D}_N{N}_P{P}")
+            traffic = None if lss else json.load(open(tp)).get(f"attn_bwd_D{D}_N{N}_P{P}")
         except Exception:
             traffic = None
     roofline = {"bound": "tensor", "kernel": "attn_bwd_kernel", "achieved": kb["tflops"],
@@ -299,8 +304,8 @@ def main():
             k_ = hk.to(dev, non_blocking=True)
             v_ = hv.to(dev, non_blocking=True)
             d_ = hd.to(dev, non_blocking=True)
-            r = ua.ulysses_attn_fwd(ctx, q_, k_, v_, out=out, lse=lse)
-            ua.ulysses_attn_bwd(ctx, q_, k_, v_, r.out, r.lse, d_, dq=dq, dk=dk, dv=dv)
+            r = fwd_fn(ctx, q_, k_, v_, out=out, lse=lse)
+            bwd_fn(ctx, q_, k_, v_, r.out, r.lse, d_, dq=dq, dk=dk, dv=dv)
             ho.copy_(out, non_blocking=True)
             hdq.copy_(dq, non_blocking=True)
             hdk.copy_(dk, non_blocking=True)
@@ -321,15 +326,16 @@ def main():
         e2e = {"value": (fwd_f + bwd_f) / (ms_e2e * 1e-3) / 1e12, "unit": UNIT, "ms_per_step": ms_e2e,
                "h2d_bytes_per_step": 4 * nbytes, "d2h_bytes_per_step": 4 * nbytes,
                "tokens_per_s": B * N / (ms_e2e * 1e-3),
-               "path": "pinned host q,k,v,dO -> H2D -> ua_ulysses_attn_fwd/bwd -> D2H out,dq,dk,dv (per rank)"}
+               "path": f"pinned host q,k,v,dO -> H2D -> ua_{args.strategy}_attn_fwd/bwd -> D2H out,dq,dk,dv (per rank)"}
 
     if rank == 0:
         res = {
             "metric": METRIC, "value": tflops, "unit": UNIT, "n_gpus": P, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": f"c4: Ulysses attention fwd+bwd, N={N} tokens, H={H}, D={D}, B={B}, P={P}",
-                       "B": B, "N": N, "H": H, "D": D, "P": P, "parallelism": f"ulysses-sp{P}", "a2a": args.a2a if P > 1 else "none",
+            "config": {"workload": f"c4: {'LSS' if lss else 'Ulysses'} attention fwd+bwd, N={N} tokens, H={H}, D={D}, B={B}, P={P}",
+                       "B": B, "N": N, "H": H, "D": D, "P": P, "parallelism": f"{args.strategy}-sp{P}",
+                       "a2a": ("nccl all-gather/reduce-scatter" if lss else args.a2a) if P > 1 else "none",
                        "l2": "inputs larger than L2 (each q/k/v/dO shard "
                              f"{q.numel() * 2 / 1e6:.0f} MB; working set > 126 MB)",
                        "inputs": "N(0,1) bf16, torch.randn seeded per rank"},

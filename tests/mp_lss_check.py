@@ -83,7 +83,10 @@ def main():
         assert np.array_equal(out_g, r1.out.float().cpu().numpy()), "P-way LSS forward != P=1 forward"
         assert np.array_equal(lse_g, r1.lse.cpu().numpy()), "P-way LSS lse != P=1 lse"
         for x, y in zip((dq_g, dk_g, dv_g), g1):
-            assert np.abs(x - y.float().cpu().numpy()).max() <= 2e-2
+            # dK, dV: fp32 partial sums vs one TMEM accumulation, each rounded to bf16
+            # once -> they may differ by an ulp (2^-7 relative) on large sigma=2 gradients
+            y = y.float().cpu().numpy()
+            assert (np.abs(x - y) - (2e-2 + 2.0 ** -7 * np.abs(y))).max() <= 0
         f64 = [synth.to_f64(t) for t in (q, k, v, do)]
         ref, ref_lse, absv = oracle.attn_fwd(*f64[:3], with_abs=True)
         gate_out(out_g, ref, gate_a=a.sigma == 1.0, absv=absv)
