@@ -155,9 +155,12 @@ ua_status make_map(CUtensorMap* m, const void* base, int D, int64_t N, int heads
                    int64_t sb, uint32_t box_rows = 128) {
   const uint64_t dims[4] = {uint64_t(D), uint64_t(N), uint64_t(heads), uint64_t(B)};
   const uint64_t strides[3] = {uint64_t(sn) * 2, uint64_t(sh) * 2, uint64_t(sb) * 2};
-  const uint32_t box0 = D >= 64 ? 64 : uint32_t(D);
-  if (!ua::make_tmap_bf16_4d(m, base, dims, strides, box0, box_rows,
-                             D >= 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B))
+  // one box per smem atom (attn_common.cuh TileGeom): 64 columns SW128 (D = 64, 128), 32 columns SW64
+  // (D = 32), 16 columns SW32 (D = 72: five atoms, columns 72..79 of the last zero-filled by TMA)
+  const uint32_t box0 = D % 64 == 0 ? 64 : (D % 32 == 0 ? 32 : 16);
+  const CUtensorMapSwizzle sw = D % 64 == 0 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                            : (D % 32 == 0 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B);
+  if (!ua::make_tmap_bf16_4d(m, base, dims, strides, box0, box_rows, sw))
     return fail(UA_ERR_CUDA, "cuTensorMapEncodeTiled failed (D=%d N=%lld heads=%d)", D, (long long)N, heads);
   return UA_OK;
 }
@@ -284,6 +287,7 @@ ua_status launch_attention_fwd(Rows q, const void* k, const void* v, Rows kv, ua
   p.kv_begin = int(kv_begin);
   p.kv_end = int(kv_end);
   p.scale_log2 = float(1.4426950408889634 / std::sqrt(double(D)));
+  p.d_io = D;
   UA_CUDA(ua::launch_attn_fwd(p, D, int(B), heads, stream));
   return UA_OK;
 }
@@ -336,6 +340,7 @@ ua_status launch_attention_bwd(Rows q, const void* dout, const void* k, const vo
   p.batch = int(B);
   p.scale = float(1.0 / std::sqrt(double(D)));
   p.scale_log2 = float(1.4426950408889634 / std::sqrt(double(D)));
+  p.d_io = D;
   UA_CUDA(ua::launch_attn_bwd(p, D, int(B), heads, stream));
   return UA_OK;
 }
@@ -448,7 +453,8 @@ ua_status ua_validate(int64_t B, int64_t N, int H, int D, int P) {
   if (P > H || H % P != 0)
     return fail(UA_ERR_HEAD_DIVISIBILITY, "Ulysses needs P <= H and H %% P == 0 (H=%d, P=%d)", H, P);
   if (N % P != 0) return fail(UA_ERR_SEQ_DIVISIBILITY, "Ulysses needs N %% P == 0 (N=%lld, P=%d)", (long long)N, P);
-  if (D != 32 && D != 64 && D != 128) return fail(UA_ERR_UNSUPPORTED, "head dim D=%d not in {32, 64, 128}", D);
+  if (D != 32 && D != 64 && D != 72 && D != 128)
+    return fail(UA_ERR_UNSUPPORTED, "head dim D=%d not in {32, 64, 72, 128}", D);
   if (N >= (int64_t(1) << 31)) return fail(UA_ERR_UNSUPPORTED, "N=%lld >= 2^31", (long long)N);
   if (B * N * H >= (int64_t(1) << 40)) return fail(UA_ERR_UNSUPPORTED, "problem too large");
   return UA_OK;
@@ -569,6 +575,8 @@ ua_status ua_ulysses_attn_fwd(ua_ctx* ctx, const void* q, const void* k, const v
                                 stream);
   }
 
+  if (ctx->a2a_mode == UA_A2A_PEER && D == 72)
+    return fail(UA_ERR_UNSUPPORTED, "peer all-to-all supports D in {32, 64, 128}; use the NCCL transport for D=72");
   if (ctx->a2a_mode == UA_A2A_PEER) {
     // Fused all-to-alls over NVLink peer stores (no NCCL on the data path).
     const size_t S = size_t(s.shard()) * 2;
@@ -694,6 +702,8 @@ ua_status ua_ulysses_attn_bwd(ua_ctx* ctx, const void* q, const void* k, const v
     return UA_OK;
   }
 
+  if (ctx->a2a_mode == UA_A2A_PEER && D == 72)
+    return fail(UA_ERR_UNSUPPORTED, "peer all-to-all supports D in {32, 64, 128}; use the NCCL transport for D=72");
   if (ctx->a2a_mode == UA_A2A_PEER) {
     // Fused all-to-alls over NVLink peer stores (no NCCL on the data path).
     const size_t S = size_t(s.shard()) * 2;
@@ -812,7 +822,8 @@ ua_status ua_lss_validate(int64_t B, int64_t N, int H, int D, int P) {
     return fail(UA_ERR_INVALID_ARG, "B, N, H, D, P must be >= 1 (got B=%lld N=%lld H=%d D=%d P=%d)", (long long)B,
                 (long long)N, H, D, P);
   if (N % P != 0) return fail(UA_ERR_SEQ_DIVISIBILITY, "LSS needs N %% P == 0 (N=%lld, P=%d)", (long long)N, P);
-  if (D != 32 && D != 64 && D != 128) return fail(UA_ERR_UNSUPPORTED, "head dim D=%d not in {32, 64, 128}", D);
+  if (D != 32 && D != 64 && D != 72 && D != 128)
+    return fail(UA_ERR_UNSUPPORTED, "head dim D=%d not in {32, 64, 72, 128}", D);
   if (N >= (int64_t(1) << 31)) return fail(UA_ERR_UNSUPPORTED, "N=%lld >= 2^31", (long long)N);
   if (B * N * H >= (int64_t(1) << 40)) return fail(UA_ERR_UNSUPPORTED, "problem too large");
   return UA_OK;

@@ -326,7 +326,7 @@ cudaError_t launch_attn_bwd(const BwdParams& p, int D, int B, int heads, cudaStr
     return e != nullptr && std::strcmp(e, "v1") == 0;
   }();
   if (!force_v1) return launch_attn_bwd_ws(p, D, stream);
-  if (p.n_kv != p.n || p.kv_f32) return cudaErrorInvalidValue;  // v1: square problems, bf16 outputs only
+  if (p.n_kv != p.n || p.kv_f32 || D == 72) return cudaErrorInvalidValue;  // v1: square, bf16 out, D in {32, 64, 128}
   switch (D) {
     case 32: return launch_bwd_impl<32>(p, B, heads, stream);
     case 64: return launch_bwd_impl<64>(p, B, heads, stream);

@@ -40,18 +40,9 @@
 #define UA_BWD_STAGGER 16   // query-tile window the persistent CTAs' start tiles are spread over
 #endif
 
-#ifndef UA_BWD_DQ_RED
-#define UA_BWD_DQ_RED 0     // dQ drain: 1 = red.global.add.v4.f32 from registers, 0 = smem box + TMA reduce-add
-#endif
-
 namespace ua {
 
 namespace {
-
-__device__ __forceinline__ void red_add_f32x4(float* addr, float a, float b, float c, float d) {
-  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b), "f"(c), "f"(d)
-               : "memory");
-}
 
 template <int D>
 struct BwdWsCfg {
@@ -66,7 +57,7 @@ struct BwdWsCfg {
   static constexpr bool kKvTmem = UA_BWD_KV_TMEM && D <= 64;
   static constexpr uint32_t kColK = 256 + 3 * D, kColV = 256 + 3 * D + D / 2;
   static constexpr int kHalfBytes = 64 * D * 2;               // one [64][D] bf16 half tile
-  static constexpr int kSlots = D == 128 ? 3 : 6;              // half-tile ring depth
+  static constexpr int kSlots = D == 128 ? 3 : (D == 80 ? 4 : 6);  // half-tile ring depth
   static constexpr int kSlotBytes = 2 * kHalfBytes;            // Q_h + dO_h
   static constexpr int kNumDs = kAliasDq ? 1 : 2;              // dS^T smem buffers
   static constexpr int kDsBytes = 128 * 128 * 2;
@@ -402,9 +393,10 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_ws_kernel(const __grid_consta
       __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(dst_v.base) + b * dst_v.sb + h * dst_v.sh +
                            int64_t(krow) * dst_v.sn;
       const PeerOut& po = hh == 0 ? p.dv_peer : p.dk_peer;
+      const int d_io = D % 32 == 0 ? D : p.d_io;  // columns >= d_io (padding of head dim 72) are not stored
       if (po.base[0] != nullptr && valid) {  // fused return all-to-all: the token owner's buffer
         const int owner = int(krow / po.nl);
-        dst = reinterpret_cast<__nv_bfloat16*>(po.base[owner]) + ((b * po.nl + (krow - owner * po.nl)) * po.H + po.h0 + h) * D;
+        dst = reinterpret_cast<__nv_bfloat16*>(po.base[owner]) + ((b * po.nl + (krow - owner * po.nl)) * po.H + po.h0 + h) * d_io;
       }
       if (p.kv_f32) {  // fp32 partial sums (LSS: reduce-scattered across ranks afterwards)
         float* fdst = reinterpret_cast<float*>(dst_v.base) + b * dst_v.sb + h * dst_v.sh + int64_t(krow) * dst_v.sn;
@@ -416,6 +408,7 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_ws_kernel(const __grid_consta
           if (valid) {
 #pragma unroll
             for (int x = 0; x < 16; x += 4)
+              if (cc + x < d_io)
               *reinterpret_cast<float4*>(fdst + cc + x) =
                   make_float4(__uint_as_float(r[x]) * sc, __uint_as_float(r[x + 1]) * sc,
                               __uint_as_float(r[x + 2]) * sc, __uint_as_float(r[x + 3]) * sc);
@@ -432,7 +425,7 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_ws_kernel(const __grid_consta
         for (int x = 0; x < 8; ++x) pk[x] = pack_bf16x2(__uint_as_float(r[2 * x]) * sc, __uint_as_float(r[2 * x + 1]) * sc);
         if (valid) {
           *reinterpret_cast<uint4*>(dst + cc) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-          *reinterpret_cast<uint4*>(dst + cc + 8) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+          if (cc + 8 < d_io) *reinterpret_cast<uint4*>(dst + cc + 8) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
         }
       }
       tc_fence_before();
@@ -444,8 +437,10 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_ws_kernel(const __grid_consta
     const int r = quad * 32 + lane;  // query row within the tile
     const bool leader = threadIdx.x == 384;
     const uint32_t t_lane = tbase + (uint32_t(quad * 32) << 16);
-    constexpr int kCols = D == 128 ? 64 : D;   // columns held in registers per round
-    constexpr int kRounds = D / kCols;
+    // columns held in registers per round; D = 80 drains 96 columns (3 boxes of 32: the
+    // TMA reduce drops columns >= 72 as out of bounds, TMEM columns 496..511 are spare)
+    constexpr int kCols = D == 128 ? 64 : (D == 80 ? 96 : D);
+    constexpr int kRounds = D == 128 ? 2 : 1;
     int T = 0;
     for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
       const int bh = item / n_kt;
@@ -471,14 +466,6 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_ws_kernel(const __grid_consta
             mbar_arrive(dq_empty);
             if (r == 0) UA_TEV(4, T, 3);
           }
-#if UA_BWD_DQ_RED
-          {  // straight from registers: fp32 vector reductions into dq_acc (no smem staging)
-            float* dst = p.dq_acc + (int64_t(bh) * n_pad + tile * 128 + r) * D + rd * kCols;
-#pragma unroll
-            for (int e = 0; e < kCols; e += 4) red_add_f32x4(dst + e, acc[e], acc[e + 1], acc[e + 2], acc[e + 3]);
-          }
-          if (false)
-#endif
           // kCols / 32 boxes through kStageBoxes staging boxes
 #pragma unroll
           for (int cb0 = 0; cb0 < kCols / 32; cb0 += C::kStageBoxes) {
@@ -544,6 +531,7 @@ cudaError_t launch_attn_bwd_ws(const BwdParams& p, int D, cudaStream_t stream) {
   switch (D) {
     case 32: return launch_bwd_ws_impl<32>(p, stream);
     case 64: return launch_bwd_ws_impl<64>(p, stream);
+    case 72: return launch_bwd_ws_impl<80>(p, stream);   // padded MMA head dim, p.d_io = 72
     case 128: return launch_bwd_ws_impl<128>(p, stream);
     default: return cudaErrorInvalidValue;
   }

@@ -11,17 +11,24 @@ namespace ua {
 
 // Per-head-dim smem tile geometry.  A [128 rows][D] bf16 tile is stored as
 // kAtoms column blocks ("atoms") of [128][kAtomCols], each row kSw bytes,
-// swizzled by TMA (SWIZZLE_128B for D >= 64, SWIZZLE_64B for D = 32).
+// swizzled by TMA: SWIZZLE_128B when 64 | D (64, 128), SWIZZLE_64B for D = 32,
+// SWIZZLE_32B for D = 80 (the padded tile of head dim 72: five 16-column
+// atoms, columns 72..79 zero-filled by TMA).  D here is the MMA head dim; the
+// I/O head dim (72 for the padded case) travels in the kernel params.
 template <int D>
 struct TileGeom {
-  static constexpr int kSw = D >= 64 ? 128 : 64;           // swizzle span (bytes per atom row)
+  static constexpr int kSw = D % 64 == 0 ? 128 : (D % 32 == 0 ? 64 : 32);  // swizzle span (bytes per atom row)
   static constexpr int kAtomCols = kSw / 2;                 // bf16 per atom row
   static constexpr int kAtoms = D / kAtomCols;              // atoms along D
   static constexpr int kAtomBytes = 128 * kSw;              // one atom of 128 rows
   static constexpr int kTileBytes = 128 * D * 2;            // whole [128][D] tile
-  static constexpr uint32_t kLayout = kSw == 128 ? 2u : 4u; // SWIZZLE_128B : SWIZZLE_64B
+  static constexpr uint32_t kLayout = kSw == 128 ? 2u : (kSw == 64 ? 4u : 6u);  // SWIZZLE_128B / 64B / 32B
   static constexpr uint32_t kSBO = 8 * kSw;                 // 8-row group stride
+  static_assert(D % 16 == 0 && kAtoms * kAtomCols == D, "head dim");
 };
+
+// MMA head dim of an I/O head dim (72 -> 80: K and N must be multiples of 16).
+constexpr int mma_dim(int d) { return (d + 15) / 16 * 16; }
 
 // Generic smem descriptor (version 1, base offset 0).
 __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout) {

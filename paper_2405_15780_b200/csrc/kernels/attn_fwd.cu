@@ -453,13 +453,21 @@ __global__ void __launch_bounds__(384, 1) attn_fwd_kernel(const __grid_constant_
         mbar_wait(&o_done[t], (j - 1) & 1);
         tc_fence_after();
 #pragma unroll
-        for (int cc = 0; cc < D; cc += 32) {
+        for (int cc = 0; cc + 32 <= D; cc += 32) {
           uint32_t r[32];
           tmem_ld32(t_lane + colO + cc, r);
           tmem_ld_wait();
 #pragma unroll
           for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
           tmem_st32(t_lane + colO + cc, r);
+        }
+        if constexpr (D % 32 != 0) {  // D = 80: the last 16 columns (never touch the next tile's O)
+          uint32_t r[16];
+          tmem_ld16(t_lane + colO + D - 16, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
+          tmem_st16(t_lane + colO + D - 16, r);
         }
       }
       if (row == 0) UA_TEV(2 + t, j, 6);
@@ -477,10 +485,12 @@ __global__ void __launch_bounds__(384, 1) attn_fwd_kernel(const __grid_constant_
     const float inv_l = 1.f / l;
     const bool valid = q_row < p.n_q;
     __nv_bfloat16* orow = reinterpret_cast<__nv_bfloat16*>(p.o.base) + b * p.o.sb + h * p.o.sh + int64_t(q_row) * p.o.sn;
+    // I/O head dim: == D except the padded D = 80 tile of head dim 72 (columns >= d_io are not stored)
+    const int d_io = D % 32 == 0 ? D : p.d_io;
     if (p.o_peer.base[0] != nullptr && valid) {  // fused return all-to-all: store into the token owner's buffer
       const int owner = int(q_row / p.o_peer.nl);
       orow = reinterpret_cast<__nv_bfloat16*>(p.o_peer.base[owner]) +
-             ((b * p.o_peer.nl + (q_row - owner * p.o_peer.nl)) * p.o_peer.H + p.o_peer.h0 + h) * D;
+             ((b * p.o_peer.nl + (q_row - owner * p.o_peer.nl)) * p.o_peer.H + p.o_peer.h0 + h) * d_io;
     }
 #pragma unroll
     for (int cc = 0; cc < D; cc += 32) {
@@ -492,9 +502,10 @@ __global__ void __launch_bounds__(384, 1) attn_fwd_kernel(const __grid_constant_
           float* frow = p.o_f32 + b * p.of_sb + h * p.of_sh + int64_t(q_row) * p.of_sn + cc;
 #pragma unroll
           for (int i = 0; i < 32; i += 4)
-            *reinterpret_cast<float4*>(frow + i) =
-                make_float4(__uint_as_float(r[i]) * inv_l, __uint_as_float(r[i + 1]) * inv_l,
-                            __uint_as_float(r[i + 2]) * inv_l, __uint_as_float(r[i + 3]) * inv_l);
+            if (cc + i < d_io)
+              *reinterpret_cast<float4*>(frow + i) =
+                  make_float4(__uint_as_float(r[i]) * inv_l, __uint_as_float(r[i + 1]) * inv_l,
+                              __uint_as_float(r[i + 2]) * inv_l, __uint_as_float(r[i + 3]) * inv_l);
         }
       } else {
         uint32_t pk[16];
@@ -504,7 +515,8 @@ __global__ void __launch_bounds__(384, 1) attn_fwd_kernel(const __grid_constant_
         if (valid) {
 #pragma unroll
           for (int i = 0; i < 16; i += 4)
-            *reinterpret_cast<uint4*>(orow + cc + 2 * i) = make_uint4(pk[i], pk[i + 1], pk[i + 2], pk[i + 3]);
+            if (cc + 2 * i < d_io)
+              *reinterpret_cast<uint4*>(orow + cc + 2 * i) = make_uint4(pk[i], pk[i + 1], pk[i + 2], pk[i + 3]);
         }
       }
     }
@@ -544,6 +556,7 @@ cudaError_t launch_attn_fwd(const FwdParams& p, int D, int B, int Hx, cudaStream
   switch (D) {
     case 32: return launch_fwd_impl<32>(p, B, Hx, stream);
     case 64: return launch_fwd_impl<64>(p, B, Hx, stream);
+    case 72: return launch_fwd_impl<80>(p, B, Hx, stream);   // padded MMA head dim, p.d_io = 72
     case 128: return launch_fwd_impl<128>(p, B, Hx, stream);
     default: return cudaErrorInvalidValue;
   }

@@ -48,6 +48,7 @@ struct alignas(64) FwdParams {
   int n_q;            // number of query rows
   int kv_begin, kv_end;  // key range; kv_begin % 128 == 0
   float scale_log2;   // log2(e) / sqrt(D)
+  int d_io;           // head dim of the I/O tensors (72 runs in the D = 80 kernel; else == D)
 };
 
 struct alignas(64) BwdParams {
@@ -73,6 +74,7 @@ struct alignas(64) BwdParams {
   int batch;
   float scale;        // 1/sqrt(D)
   float scale_log2;   // log2(e)/sqrt(D)
+  int d_io;           // head dim of the I/O tensors and of dq_acc rows (72 runs in the D = 80 kernel)
 };
 
 cudaError_t launch_attn_fwd(const FwdParams& p, int D, int B, int heads, cudaStream_t stream);

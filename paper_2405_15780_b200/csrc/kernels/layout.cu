@@ -63,6 +63,34 @@ __global__ void __launch_bounds__(256) pack_kernel(Ptrs4 ptrs, int ntensors, int
   }
 }
 
+// Delta = sum_d dO.O in fp32 for one (b, t, h) row per thread (head dims whose
+// row is not a power-of-two number of 16-B vectors, e.g. D = 72); same
+// destination index as pack_kernel's fused Delta.
+__global__ void __launch_bounds__(256) delta_kernel(int64_t B, int64_t Nl, int H, int Hl, int vpr,
+                                                    const uint4* __restrict__ dout, const uint4* __restrict__ out,
+                                                    float* __restrict__ delta) {
+  const int64_t rows = B * Nl * H;
+  for (int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < rows; r += int64_t(gridDim.x) * blockDim.x) {
+    const int h = int(r % H);
+    const int64_t t = (r / H) % Nl;
+    const int64_t b = r / (int64_t(H) * Nl);
+    const int j = h / Hl, hp = h % Hl;
+    float acc = 0.f;
+    for (int i = 0; i < vpr; ++i) {
+      uint4 a = dout[r * vpr + i], o = out[r * vpr + i];
+      const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&a);
+      const __nv_bfloat162* o2 = reinterpret_cast<const __nv_bfloat162*>(&o);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        float2 fa = __bfloat1622float2(a2[k]), fo = __bfloat1622float2(o2[k]);
+        acc = fmaf(fa.x, fo.x, acc);
+        acc = fmaf(fa.y, fo.y, acc);
+      }
+    }
+    delta[((int64_t(j) * Nl + t) * B + b) * Hl + hp] = acc;
+  }
+}
+
 template <int VPR>
 __global__ void __launch_bounds__(256) unpack_kernel(Ptrs4 ptrs, int ntensors, int64_t B, int64_t Nl, int H, int Hl) {
   const int64_t total = B * Nl * H * VPR;
@@ -162,6 +190,11 @@ cudaError_t launch_pack(const void* const* src, void* const* dst, int ntensors, 
     case 4: pack_kernel<4><<<grid, 256, 0, stream>>>(ptrs, ntensors, B, Nl, H, Hl, dv, ov, delta_dst); break;
     case 8: pack_kernel<8><<<grid, 256, 0, stream>>>(ptrs, ntensors, B, Nl, H, Hl, dv, ov, delta_dst); break;
     case 16: pack_kernel<16><<<grid, 256, 0, stream>>>(ptrs, ntensors, B, Nl, H, Hl, dv, ov, delta_dst); break;
+    case 9:  // D = 72: rows of 9 vectors straddle warps, Delta in its own pass
+      if (ntensors > 0) pack_kernel<9><<<grid, 256, 0, stream>>>(ptrs, ntensors, B, Nl, H, Hl, nullptr, nullptr, nullptr);
+      if (delta_dst != nullptr)
+        delta_kernel<<<grid_for(B * Nl * H, 256), 256, 0, stream>>>(B, Nl, H, Hl, 9, dv, ov, delta_dst);
+      break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
@@ -182,6 +215,7 @@ cudaError_t launch_unpack(const void* const* src, void* const* dst, int ntensors
     case 4: unpack_kernel<4><<<grid, 256, 0, stream>>>(ptrs, ntensors, B, Nl, H, Hl); break;
     case 8: unpack_kernel<8><<<grid, 256, 0, stream>>>(ptrs, ntensors, B, Nl, H, Hl); break;
     case 16: unpack_kernel<16><<<grid, 256, 0, stream>>>(ptrs, ntensors, B, Nl, H, Hl); break;
+    case 9: unpack_kernel<9><<<grid, 256, 0, stream>>>(ptrs, ntensors, B, Nl, H, Hl); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();

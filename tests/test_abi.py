@@ -50,7 +50,9 @@ def test_version_and_status_strings():
     ((1, 16, 4, 64, 8), 2),      # H=4, P=8 -> HeadDivisibility
     ((1, 12, 6, 64, 4), 2),      # P does not divide H
     ((1, 10, 4, 64, 4), 3),      # N % P != 0 -> SeqDivisibility
-    ((1, 16, 4, 72, 2), 4),      # D=72 unsupported (Table 1 ViT-10B: NEXT)
+    ((1, 16, 4, 72, 2), 0),      # D=72: ViT-10B, 4608 / 64 heads (Table 1)
+    ((1, 16, 4, 80, 2), 4),      # D=80 unsupported
+    ((1, 16, 4, 160, 2), 4),     # D=160 (2560 / 16) unsupported: TMEM cannot hold S and two O tiles
     ((0, 16, 4, 64, 1), 1),
     ((1, 0, 4, 64, 1), 1),
     ((1, 1 << 31, 32, 64, 8), 4),
@@ -101,7 +103,8 @@ def test_no_cpu_fallback():
     ((1, 16, 4, 64, 8), 0),       # LSS has no head limit: H=4, P=8 is fine
     ((1, 12, 6, 64, 4), 0),       # P need not divide H
     ((1, 10, 4, 64, 4), 3),       # N % P != 0 -> SeqDivisibility
-    ((1, 16, 4, 72, 2), 4),
+    ((1, 16, 4, 72, 2), 0),
+    ((1, 16, 4, 96, 2), 4),
     ((0, 16, 4, 64, 1), 1),
     ((1, 188416, 32, 64, 8), 0),
     ((1, 1048576, 32, 128, 64), 0),

@@ -55,6 +55,9 @@ def check(ua, ctx, B, N, H, D, sigma, seed):
     (1000, 2, 128, 2.0),
     (4050, 2, 64, 1.0),     # P:263 seq 4050 (ragged tail)
     (2048, 2, 32, 2.0),
+    (300, 2, 72, 1.0),      # D=72 (ViT-10B)
+    (1000, 3, 72, 2.0),
+    (129, 2, 72, 1.0),
 ])
 def test_bwd_parity_small(ua, ctx, N, H, D, sigma):
     check(ua, ctx, 1, N, H, D, sigma, seed=100 + N)

@@ -43,6 +43,9 @@ def run_fwd(ua, ctx, q, k, v):
     (1000, 2, 128, 2.0),    # ragged, D=128
     (4050, 2, 64, 1.0),     # P:263 seq 4050
     (2048, 2, 32, 2.0),
+    (300, 2, 72, 1.0),      # D=72 (ViT-10B): padded 80-wide MMA tiles, SW32 atoms
+    (1000, 3, 72, 2.0),
+    (129, 2, 72, 1.0),
 ])
 def test_fwd_parity_small(ua, ctx, N, H, D, sigma):
     q, k, v = synth.qkv(1, N, H, D, seed=7 + N, sigma_qk=sigma)
@@ -118,3 +121,18 @@ def test_fwd_c4_sampled_rows(ua, ctx):
     gate_out(out[0, idx, bh[:, 1]], o_r)
     gate_lse(lse[0, bh[:, 1], idx], l_r)
     assert np.isfinite(out).all()
+
+
+@pytest.mark.parametrize("D", [32, 64, 72, 128])
+def test_fwd_lazy_rescale_ramp(ua, ctx, D):
+    """Keys whose norms grow along the sequence make every query's running max
+    rise tile after tile, so the lazy O / l rescale (threshold 2^8) fires often
+    in both query tiles of a CTA; the result must still be the exact softmax."""
+    N, H = 1536, 2
+    q, k, v = synth.qkv(1, N, H, D, seed=31, sigma_qk=1.0)
+    ramp = torch.linspace(0.2, 3.0, N).view(1, N, 1, 1)
+    k = (k.float() * ramp).to(torch.bfloat16)          # deterministic transform of synth inputs
+    out, lse = run_fwd(ua, ctx, q, k, v)
+    ref, ref_lse, absv = oracle.attn_fwd(synth.to_f64(q), synth.to_f64(k), synth.to_f64(v), with_abs=True)
+    gate_out(out, ref, gate_a=False, absv=absv)
+    gate_lse(lse, ref_lse)
