@@ -51,7 +51,7 @@ typedef enum {
   UA_ERR_INVALID_ARG = 1,       /* null / misaligned pointer, non-positive size, P != ctx P, workspace too small */
   UA_ERR_HEAD_DIVISIBILITY = 2, /* P > H or H % P != 0 (P:317 head limit) */
   UA_ERR_SEQ_DIVISIBILITY = 3,  /* N % P != 0; no padding */
-  UA_ERR_UNSUPPORTED = 4,       /* D not in {32, 64, 128}; N >= 2^31; no sm_100 device */
+  UA_ERR_UNSUPPORTED = 4,       /* D not in {32, 64, 72, 128}; N >= 2^31; no sm_100 device; D = 72 with the peer transport */
   UA_ERR_CUDA = 5,
   UA_ERR_NCCL = 6
 } ua_status;
@@ -184,7 +184,7 @@ ua_status ua_f32_to_bf16_bnhd(const float* src, void* dst, int64_t B, int64_t N,
  * reduce-scatter); 0 at P = 1, where both reduce to plain attention.
  *   q, k, v, out, dout, dq, dk, dv : bf16 [B][N/P][H][D] (sequence shard)
  *   lse : fp32 [B][H][N/P]   (this rank's queries, all heads)
- * Constraints: N % P == 0, D in {32, 64, 128}; any H >= 1 and any P (P > H is
+ * Constraints: N % P == 0, D in {32, 64, 72, 128}; any H >= 1 and any P (P > H is
  * allowed).  Same ownership / async / collective conventions as above.
  * Collective calls and bytes are counted in ua_ctx_comm_stats. */
 ua_status ua_lss_validate(int64_t B, int64_t N, int H, int D, int P);
