@@ -195,6 +195,34 @@ ua_status ua_lss_attn_bwd(ua_ctx* ctx, const void* q, const void* k, const void*
                           const void* dout, void* dq, void* dk, void* dv, int64_t B, int64_t N, int H, int D, int P,
                           void* workspace, size_t workspace_bytes, ua_stream_t stream);
 
+/* ------------------------------------------------------------- attention layer
+ * The rest of the paper's attention layer around the Ulysses attention
+ * (SURVEY §8(f)-3): the Q/K/V and output projections and the SP group's
+ * weight-gradient all-reduce (§5.4, §6.1: "two all-to-all
+ * calls in the forward pass and two all-to-all calls + all reduce in the
+ * backward pass per layer").  Reading (R16): bias-free projections,
+ * y = x W^T, E = H * D, M = B * N/P tokens of this rank:
+ *   forward   q|k|v = x Wq^T | x Wk^T | x Wv^T;  o = Ulysses attention;  y = o Wo^T
+ *   backward  do = dy Wo, dWo = dy^T o;  (dq, dk, dv) = attention backward;
+ *             dx = dq Wq + dk Wk + dv Wv;  dW_qkv = [dq^T x; dk^T x; dv^T x];
+ *             dW_qkv and dWo summed over the P ranks (ONE fused NCCL all-reduce).
+ *   x, y, dy, dx : bf16 [B][N/P][E]        (sequence shard)
+ *   w_qkv        : bf16 [3E][E]            (rows: Wq, Wk, Wv; head h = rows h*D..h*D+D-1 of each)
+ *   w_o          : bf16 [E][E]
+ *   dw_qkv, dw_o : fp32 [3E][E], [E][E]    (full gradients, identical on every rank)
+ *   saved        : caller-owned, ua_layer_sizes' saved_bytes: q, k, v, o, lse of the forward
+ * GEMMs: cuBLASLt, bf16 operands, fp32 accumulation (plain library GEMMs).
+ * Collective calls per step: 2 forward, 3 backward (counted by ua_ctx_comm_stats).
+ * Same validation (ua_validate) and conventions as the attention entry points. */
+ua_status ua_layer_sizes(int64_t B, int64_t N, int H, int D, int P, size_t* saved_bytes, size_t* fwd_bytes,
+                         size_t* bwd_bytes);
+ua_status ua_layer_fwd(ua_ctx* ctx, const void* x, const void* w_qkv, const void* w_o, void* y, void* saved,
+                       int64_t B, int64_t N, int H, int D, int P, void* workspace, size_t workspace_bytes,
+                       ua_stream_t stream);
+ua_status ua_layer_bwd(ua_ctx* ctx, const void* x, const void* w_qkv, const void* w_o, const void* saved,
+                       const void* dy, void* dx, float* dw_qkv, float* dw_o, int64_t B, int64_t N, int H, int D, int P,
+                       void* workspace, size_t workspace_bytes, ua_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -12,7 +12,10 @@ Contents
     sequence shards, the all-to-all, head shards, and the
     composition seq-shard -> a2a -> per-head attention -> a2a back.
   * ``lss`` — contiguous key-segment attention and the exact log-sum-exp merge
-    of partial results ("LSS chunking" in BASELINE.json).
+    of partial results ("LSS chunking" in BASELINE.json), and the
+    LSS sequence-parallel strategy (per-rank forward, partial dK/dV, reduce).
+  * ``layer`` — the attention layer around it: bias-free Q/K/V and output
+    projections and their gradients.
 
 Parity status: every function is pinned by ``tests/test_oracle.py`` (numpy
 brute force on materialised N x N, central finite differences, closed forms
@@ -139,4 +142,4 @@ def attn_bwd(q, k, v, dout, with_abs: bool = False):
     return dq, dk, dv, out, lse
 
 
-from . import lss, ulysses  # noqa: E402,F401
+from . import layer, lss, ulysses  # noqa: E402,F401

@@ -30,7 +30,8 @@ EXPORTS = ("ua_version", "ua_status_string", "ua_last_error", "ua_validate", "ua
            "ua_get_unique_id", "ua_ctx_create", "ua_ctx_destroy", "ua_ctx_comm_stats",
            "ua_ctx_enable_timing", "ua_ctx_phase_times", "ua_ctx_set_a2a_mode", "ua_ctx_get_a2a_mode",
            "ua_ulysses_attn_fwd", "ua_ulysses_attn_bwd", "ua_attn_fwd_segment", "ua_lse_merge",
-           "ua_f32_to_bf16_bnhd", "ua_lss_validate", "ua_lss_workspace_size", "ua_lss_attn_fwd", "ua_lss_attn_bwd")
+           "ua_f32_to_bf16_bnhd", "ua_lss_validate", "ua_lss_workspace_size", "ua_lss_attn_fwd", "ua_lss_attn_bwd",
+           "ua_layer_sizes", "ua_layer_fwd", "ua_layer_bwd")
 
 PHASES = ("pack_fwd", "a2a_fwd_in", "attn_fwd", "a2a_fwd_out", "unpack_fwd", "pack_bwd", "a2a_bwd_in",
           "attn_bwd", "dq_finalize", "a2a_bwd_out", "unpack_bwd")
@@ -82,6 +83,9 @@ def lib():
         L.ua_lss_workspace_size.argtypes = [i64, i64, i32, i32, i32, ctypes.POINTER(sz), ctypes.POINTER(sz)]
         L.ua_lss_attn_fwd.argtypes = [vp, vp, vp, vp, vp, vp, i64, i64, i32, i32, i32, vp, sz, vp]
         L.ua_lss_attn_bwd.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, i64, i64, i32, i32, i32, vp, sz, vp]
+        L.ua_layer_sizes.argtypes = [i64, i64, i32, i32, i32, ctypes.POINTER(sz), ctypes.POINTER(sz), ctypes.POINTER(sz)]
+        L.ua_layer_fwd.argtypes = [vp, vp, vp, vp, vp, vp, i64, i64, i32, i32, i32, vp, sz, vp]
+        L.ua_layer_bwd.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp, i64, i64, i32, i32, i32, vp, sz, vp]
         L.ua_attn_fwd_segment.argtypes = [vp, vp, vp, vp, vp, i64, i64, i32, i32, i64, i64, vp]
         L.ua_lse_merge.argtypes = [vp, vp, vp, vp, i64, i32, vp]
         L.ua_f32_to_bf16_bnhd.argtypes = [vp, vp, i64, i64, i32, i32, vp]
@@ -293,6 +297,49 @@ def lss_attn_bwd(ctx: Context, q, k, v, out, lse, dout, dq=None, dk=None, dv=Non
     _check(lib().ua_lss_attn_bwd(ctx.handle, _ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(lse), _ptr(dout), _ptr(dq),
                                  _ptr(dk), _ptr(dv), B, N, H, D, P, _ptr(ws), ws.numel(), _stream(stream)))
     return dq, dk, dv
+
+
+def layer_sizes(B: int, N: int, H: int, D: int, P: int) -> tuple[int, int, int]:
+    """(saved_bytes, fwd_workspace_bytes, bwd_workspace_bytes) of the attention layer."""
+    a, f, b = ctypes.c_size_t(0), ctypes.c_size_t(0), ctypes.c_size_t(0)
+    _check(lib().ua_layer_sizes(B, N, H, D, P, ctypes.byref(a), ctypes.byref(f), ctypes.byref(b)))
+    return a.value, f.value, b.value
+
+
+def layer_fwd(ctx: Context, x, w_qkv, w_o, H: int, stream=None):
+    """Attention layer forward on this rank's sequence shard x bf16 [B][N/P][E]
+    (E = H*D; w_qkv [3E][E], w_o [E][E] bf16).  Returns (y, saved); saved is the
+    opaque uint8 buffer the backward needs."""
+    _need_cuda_bf16(x, w_qkv, w_o)
+    B, Nl, E = x.shape
+    D = E // H
+    P = ctx.P
+    N = Nl * P
+    sb, fb, _ = layer_sizes(B, N, H, D, P)
+    saved = torch.empty(sb, dtype=torch.uint8, device=x.device)
+    y = torch.empty_like(x)
+    ws = ctx.workspace(fb)
+    _check(lib().ua_layer_fwd(ctx.handle, _ptr(x), _ptr(w_qkv), _ptr(w_o), _ptr(y), _ptr(saved), B, N, H, D, P,
+                              _ptr(ws), ws.numel(), _stream(stream)))
+    return y, saved
+
+
+def layer_bwd(ctx: Context, x, w_qkv, w_o, saved, dy, H: int, stream=None):
+    """Attention layer backward: (dx bf16 [B][N/P][E], dw_qkv fp32 [3E][E], dw_o fp32 [E][E]);
+    the weight gradients are summed over the SP group (one all-reduce)."""
+    _need_cuda_bf16(x, w_qkv, w_o, dy)
+    B, Nl, E = x.shape
+    D = E // H
+    P = ctx.P
+    N = Nl * P
+    _, _, bb = layer_sizes(B, N, H, D, P)
+    dx = torch.empty_like(x)
+    dw_qkv = torch.empty((3 * E, E), dtype=torch.float32, device=x.device)
+    dw_o = torch.empty((E, E), dtype=torch.float32, device=x.device)
+    ws = ctx.workspace(bb)
+    _check(lib().ua_layer_bwd(ctx.handle, _ptr(x), _ptr(w_qkv), _ptr(w_o), _ptr(saved), _ptr(dy), _ptr(dx),
+                              _ptr(dw_qkv), _ptr(dw_o), B, N, H, D, P, _ptr(ws), ws.numel(), _stream(stream)))
+    return dx, dw_qkv, dw_o
 
 
 def attn_fwd_segment(q, k, v, kv_begin: int, kv_end: int, o_seg=None, lse_seg=None, stream=None):

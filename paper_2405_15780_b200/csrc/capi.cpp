@@ -15,45 +15,8 @@
 #include <string>
 #include <vector>
 
-#include "kernels/attn_kernels.h"
+#include "capi_internal.h"
 #include "tma_host.h"
-
-struct ua_ctx {
-  int P = 1;
-  int rank = 0;
-  int device = 0;
-  ncclComm_t comm = nullptr;
-  int64_t a2a_calls = 0;
-  int64_t a2a_bytes = 0;
-  // phase timing
-  bool timing = false;
-  struct Rec {
-    int phase;
-    cudaEvent_t a, b;
-  };
-  std::vector<Rec> pending;
-  std::vector<cudaEvent_t> pool;
-  // NVLink peer-store all-to-all (UA_A2A_PEER): library-owned buffers, CUDA IPC
-  // mapped on every rank (peer[k] = rank k's copy, peer[rank] = local).
-  int a2a_mode = UA_A2A_NCCL;
-  struct PeerBuf {
-    void* local = nullptr;
-    size_t bytes = 0;
-    void* peer[ua::kMaxPeers] = {};
-  };
-  PeerBuf flags, fwd_in, fwd_out, bwd_in, bwd_out;
-  int64_t step_fwd = 0, step_bwd = 0;
-  cudaEvent_t get_event() {
-    if (!pool.empty()) {
-      cudaEvent_t e = pool.back();
-      pool.pop_back();
-      return e;
-    }
-    cudaEvent_t e = nullptr;
-    cudaEventCreate(&e);
-    return e;
-  }
-};
 
 namespace {
 // RAII phase marker: records an event pair around a phase when timing is on.
@@ -79,9 +42,10 @@ struct Phase {
 }  // namespace
 
 namespace {
-
 thread_local std::string g_err;
+}  // namespace
 
+namespace ua_internal {
 ua_status fail(ua_status s, const char* fmt, ...) {
   char buf[512];
   va_list ap;
@@ -91,24 +55,10 @@ ua_status fail(ua_status s, const char* fmt, ...) {
   g_err = buf;
   return s;
 }
+}  // namespace ua_internal
 
-#define UA_CUDA(expr)                                                                       \
-  do {                                                                                      \
-    cudaError_t e_ = (expr);                                                                \
-    if (e_ != cudaSuccess) return fail(UA_ERR_CUDA, "%s: %s", #expr, cudaGetErrorString(e_)); \
-  } while (0)
-
-#define UA_NCCL(expr)                                                                        \
-  do {                                                                                       \
-    ncclResult_t r_ = (expr);                                                                \
-    if (r_ != ncclSuccess) return fail(UA_ERR_NCCL, "%s: %s", #expr, ncclGetErrorString(r_)); \
-  } while (0)
-
-#define UA_TRY(expr)                  \
-  do {                                \
-    ua_status s_ = (expr);            \
-    if (s_ != UA_OK) return s_;       \
-  } while (0)
+namespace {
+using ua_internal::fail;
 
 constexpr size_t kAlign = 256;
 size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
@@ -531,6 +481,7 @@ ua_status ua_ctx_destroy(ua_ctx* ctx) {
     cudaDeviceSynchronize();
     for (auto* pb : {&ctx->flags, &ctx->fwd_in, &ctx->fwd_out, &ctx->bwd_in, &ctx->bwd_out}) peer_release(ctx, *pb);
   }
+  ua_internal::layer_release(ctx);
   ncclResult_t r = ncclSuccess;
   if (ctx->comm) r = ncclCommDestroy(ctx->comm);
   for (auto& rec : ctx->pending) {

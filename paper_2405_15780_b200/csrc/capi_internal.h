@@ -1,0 +1,78 @@
+// capi_internal.h — definitions shared by the C ABI translation units
+// (capi.cpp: attention entry points; layer.cpp: the projection layer).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "../../include/ulysses_attn.h"
+#include "kernels/attn_kernels.h"
+
+struct ua_ctx {
+  int P = 1;
+  int rank = 0;
+  int device = 0;
+  ncclComm_t comm = nullptr;
+  int64_t a2a_calls = 0;
+  int64_t a2a_bytes = 0;
+  // phase timing
+  bool timing = false;
+  struct Rec {
+    int phase;
+    cudaEvent_t a, b;
+  };
+  std::vector<Rec> pending;
+  std::vector<cudaEvent_t> pool;
+  // NVLink peer-store all-to-all (UA_A2A_PEER): library-owned buffers, CUDA IPC
+  // mapped on every rank (peer[k] = rank k's copy, peer[rank] = local).
+  int a2a_mode = UA_A2A_NCCL;
+  struct PeerBuf {
+    void* local = nullptr;
+    size_t bytes = 0;
+    void* peer[ua::kMaxPeers] = {};
+  };
+  PeerBuf flags, fwd_in, fwd_out, bwd_in, bwd_out;
+  void* lt = nullptr;  // cublasLtHandle_t of the projection layer (layer.cpp), created on first use
+  int64_t step_fwd = 0, step_bwd = 0;
+  cudaEvent_t get_event() {
+    if (!pool.empty()) {
+      cudaEvent_t e = pool.back();
+      pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+  }
+};
+
+
+namespace ua_internal {
+// Thread-local error detail + status (ua_last_error).
+ua_status fail(ua_status s, const char* fmt, ...);
+// Releases the projection layer's cuBLASLt handle (layer.cpp); called by ua_ctx_destroy.
+void layer_release(ua_ctx* ctx);
+}  // namespace ua_internal
+
+#define UA_CUDA(expr)                                                                                    \
+  do {                                                                                                   \
+    cudaError_t e_ = (expr);                                                                             \
+    if (e_ != cudaSuccess) return ua_internal::fail(UA_ERR_CUDA, "%s: %s", #expr, cudaGetErrorString(e_)); \
+  } while (0)
+
+#define UA_NCCL(expr)                                                                                     \
+  do {                                                                                                    \
+    ncclResult_t r_ = (expr);                                                                             \
+    if (r_ != ncclSuccess) return ua_internal::fail(UA_ERR_NCCL, "%s: %s", #expr, ncclGetErrorString(r_)); \
+  } while (0)
+
+#define UA_TRY(expr)            \
+  do {                          \
+    ua_status s_ = (expr);      \
+    if (s_ != UA_OK) return s_; \
+  } while (0)

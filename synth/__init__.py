@@ -16,7 +16,8 @@ Recipe (DESIGN.md "Input recipe"):
     global tensor (c5 is 4.3e9 values per tensor); the data are identical for
     every P.
   * Seeds: BASE_SEED = 1234 (offset by the test's seed); tensor ids q=0, k=1,
-    v=2, dO=3.
+    v=2, dO=3; the attention layer's x=4, dy=5 (N(0,1), [B][N][E]) and weights
+    w_qkv=6, w_o=7 (N(0, 1/E), so the projected q, k, v have unit scale).
   * Shapes follow BASELINE.json configs (c1..c5); the paper's 188,416-token
     workload is 92 channels x 2,048 patches.
 """
@@ -25,7 +26,7 @@ from __future__ import annotations
 import numpy as np
 import torch
 
-TENSOR_IDS = {"q": 0, "k": 1, "v": 2, "do": 3}
+TENSOR_IDS = {"q": 0, "k": 1, "v": 2, "do": 3, "x": 4, "dy": 5, "w_qkv": 6, "w_o": 7}
 BASE_SEED = 1234
 BLOCK = 1024
 
@@ -92,3 +93,15 @@ def qkv(B, N, H, D, seed: int = BASE_SEED, sigma_qk: float = 1.0, with_do: bool 
 def to_f64(x: torch.Tensor) -> np.ndarray:
     """Exact widening of bf16 values to float64 numpy (for the oracle)."""
     return x.to(torch.float64).numpy()
+
+
+def layer_inputs(B, N, H, D, seed: int = BASE_SEED, n0: int = 0, n1: int | None = None):
+    """Attention-layer inputs (bf16 CPU): x, dy [B][n1-n0][E] (tokens [n0, n1)
+    of the global sequence), w_qkv [3E][E], w_o [E][E]; E = H * D."""
+    E = H * D
+    n1 = N if n1 is None else n1
+    x = normal_bf16(B, N, 1, E, seed, "x", n0=n0, n1=n1).reshape(B, n1 - n0, E)
+    dy = normal_bf16(B, N, 1, E, seed, "dy", n0=n0, n1=n1).reshape(B, n1 - n0, E)
+    w_qkv = normal_bf16(1, 3 * E, 1, E, seed, "w_qkv", sigma=E ** -0.5).reshape(3 * E, E)
+    w_o = normal_bf16(1, E, 1, E, seed, "w_o", sigma=E ** -0.5).reshape(E, E)
+    return x, dy, w_qkv, w_o

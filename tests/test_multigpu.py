@@ -61,6 +61,16 @@ def test_lss_p_way(P, B, N, H, D, sigma):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("P,N,H,D", [(2, 1024, 4, 64), (4, 2048, 8, 64), (2, 600, 2, 72)])
+def test_layer_p_way(P, N, H, D):
+    """Attention layer: projections + Ulysses + the weight-gradient all-reduce."""
+    if torch.cuda.device_count() < P:
+        pytest.skip(f"needs {P} GPUs")
+    r = torchrun(P, os.path.join(ROOT, "tests", "mp_layer_check.py"), f"--N={N}", f"--H={H}", f"--D={D}")
+    assert r.returncode == 0 and "LAYER_OK" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
+
+
+@pytest.mark.gpu
 @pytest.mark.slow
 @pytest.mark.parametrize("config,P,mode", [("c3", 1, "nccl"), ("c4", 1, "nccl"),
                                            ("c3", 2, "nccl"), ("c3", 4, "nccl"), ("c3", 8, "nccl"),

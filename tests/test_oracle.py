@@ -13,7 +13,7 @@ import pytest
 import torch
 
 import oracle
-from oracle import lss, ulysses
+from oracle import layer, lss, ulysses
 
 GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))
 
@@ -360,3 +360,38 @@ def test_bwd_dq_rows_matches_dense():
     idx = np.array([0, 69, 33, 5])
     got = oracle.attn_bwd_dq_rows(q[bh[:, 0], idx, bh[:, 1]], do[bh[:, 0], idx, bh[:, 1]], bh, k, v)
     assert np.abs(got - dq[bh[:, 0], idx, bh[:, 1]]).max() < 1e-13
+
+
+# ------------------------------------------------------------------ layer pins
+@pytest.mark.parametrize("B,N,H,D", [(1, 12, 2, 4), (2, 7, 3, 2)])
+def test_layer_matches_torch_autograd(B, N, H, D):
+    """oracle.layer (numpy matmuls + oracle.c attention) against torch fp64
+    autograd through matmuls and scaled_dot_product_attention (library routines)."""
+    import torch
+    E = H * D
+    x, dy = rnd((B, N, E), 130), rnd((B, N, E), 131)
+    w_qkv, w_o = rnd((3 * E, E), 132, 0.5), rnd((E, E), 133, 0.5)
+    y, _ = layer.layer_fwd(x, w_qkv, w_o, H)
+    dx, dwq, dwo = layer.layer_bwd(x, w_qkv, w_o, dy, H)
+    tx, twq, two = (torch.tensor(t, dtype=torch.float64, requires_grad=True) for t in (x, w_qkv, w_o))
+    qkv = [(tx @ twq[i * E:(i + 1) * E].T).reshape(B, N, H, D).transpose(1, 2) for i in range(3)]
+    o = torch.nn.functional.scaled_dot_product_attention(*qkv).transpose(1, 2).reshape(B, N, E)
+    ty = o @ two.T
+    ty.backward(torch.tensor(dy, dtype=torch.float64))
+    assert np.abs(y - ty.detach().numpy()).max() < 1e-12
+    for a, b in ((dx, tx.grad), (dwq, twq.grad), (dwo, two.grad)):
+        assert np.abs(a - b.numpy()).max() < 1e-11
+
+
+def test_layer_weight_grads_are_sums_over_tokens():
+    """The SP all-reduce sums per-shard weight gradients: the gradient
+    of a token-sharded layer's weights equals the sum over shards' own."""
+    B, N, H, D, P = 1, 12, 2, 4, 3
+    E = H * D
+    x, dy = rnd((B, N, E), 140), rnd((B, N, E), 141)
+    w_qkv, w_o = rnd((3 * E, E), 142, 0.5), rnd((E, E), 143, 0.5)
+    _, dwq, dwo = layer.layer_bwd(x, w_qkv, w_o, dy, H)
+    _, (q, k, v, o, _) = layer.layer_fwd(x, w_qkv, w_o, H)
+    Nl = N // P
+    parts = [np.einsum("bnj,bni->ji", dy[:, r * Nl:(r + 1) * Nl], o[:, r * Nl:(r + 1) * Nl]) for r in range(P)]
+    assert np.abs(sum(parts) - dwo).max() < 1e-12
