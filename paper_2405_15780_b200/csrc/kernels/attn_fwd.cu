@@ -33,6 +33,9 @@
 
 // Tuning knobs (defaults are the shipped configuration; scripts/ab.py builds
 // variants with -D overrides).
+#ifndef UA_FWD_SPLIT
+#define UA_FWD_SPLIT 1      // D <= 64: the column-split kernel of attn_fwd_split.cu (4 softmax warpgroups)
+#endif
 #ifndef UA_FWD_SEP_P
 #define UA_FWD_SEP_P 1      // separate TMEM P buffers when D <= 64: the next Q K^T overlaps this tile's softmax
 #endif
@@ -553,6 +556,9 @@ cudaError_t launch_fwd_impl(const FwdParams& p, int B, int Hx, cudaStream_t stre
 }  // namespace
 
 cudaError_t launch_attn_fwd(const FwdParams& p, int D, int B, int Hx, cudaStream_t stream) {
+#if UA_FWD_SPLIT
+  if (D <= 64) return launch_attn_fwd_split(p, D, B, Hx, stream);   // column-split softmax (attn_fwd_split.cu)
+#endif
   switch (D) {
     case 32: return launch_fwd_impl<32>(p, B, Hx, stream);
     case 64: return launch_fwd_impl<64>(p, B, Hx, stream);

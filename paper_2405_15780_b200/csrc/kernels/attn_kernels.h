@@ -78,6 +78,8 @@ struct alignas(64) BwdParams {
 };
 
 cudaError_t launch_attn_fwd(const FwdParams& p, int D, int B, int heads, cudaStream_t stream);
+// D <= 64 column-split forward (attn_fwd_split.cu); launch_attn_fwd dispatches to it when enabled.
+cudaError_t launch_attn_fwd_split(const FwdParams& p, int D, int B, int heads, cudaStream_t stream);
 cudaError_t launch_attn_bwd(const BwdParams& p, int D, int B, int heads, cudaStream_t stream);
 cudaError_t launch_attn_bwd_ws(const BwdParams& p, int D, cudaStream_t stream);
 
