@@ -180,6 +180,8 @@ def main():
     ap.add_argument("--a2a", default="nccl", choices=["nccl", "peer"],
                     help="all-to-all transport for P > 1: NCCL send/recv, or NVLink peer stores from the kernels")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--deterministic", action="store_true",
+                    help="bitwise-reproducible backward (query-stationary dQ kernel; same algorithmic flop count)")
     ap.add_argument("--strategy", default="ulysses", choices=["ulysses", "lss"],
                     help="sequence-parallel strategy: Ulysses all-to-all (headline) or LSS gather-KV / reduce-scatter")
     args = ap.parse_args()
@@ -207,6 +209,8 @@ def main():
     ctx = ua.Context(P=P, rank=rank, device=local)
     if P > 1 and not lss:
         ctx.set_a2a_mode(args.a2a)
+    if args.deterministic:
+        ctx.set_deterministic(True)
     dev = torch.device("cuda", local)
     g = torch.Generator(device=dev).manual_seed(1234 + rank)
     shape = (B, Nl, H, D)
@@ -373,7 +377,8 @@ def main():
                        "a2a": ("nccl all-gather/reduce-scatter" if lss else args.a2a) if P > 1 else "none",
                        "l2": "inputs larger than L2 (each q/k/v/dO shard "
                              f"{q.numel() * 2 / 1e6:.0f} MB; working set > 126 MB)",
-                       "inputs": "N(0,1) bf16, torch.randn seeded per rank"},
+                       "inputs": "N(0,1) bf16, torch.randn seeded per rank",
+                       "deterministic_bwd": bool(args.deterministic)},
             "tokens_per_s": B * N / (ms_step * 1e-3),
             "pct_of_bf16_peak": tflops / (P * peaks["bf16_sustained"]) * 100,
             "pct_of_bf16_burst_peak": tflops / (P * peaks["bf16_burst"]) * 100,

@@ -125,6 +125,24 @@ ua_status ua_ctx_enable_timing(ua_ctx* ctx, int enable);
 enum { UA_A2A_NCCL = 0, UA_A2A_PEER = 1 };
 ua_status ua_ctx_set_a2a_mode(ua_ctx* ctx, int mode);
 ua_status ua_ctx_get_a2a_mode(const ua_ctx* ctx, int* mode);
+
+/* Deterministic backward (in the first pass
+ * "all matrices are the same" between the sequence-parallel and the
+ * single-GPU run).  enable = 0 (default): dQ partial sums of the key tiles
+ * are reduce-added into an fp32 accumulator by concurrent CTAs, so dQ may
+ * differ in the last bits run to run.  enable != 0: dK, dV come from the
+ * KV-stationary kernel without its dQ GEMM, and a second, query-stationary
+ * kernel recomputes S and dP and sums dQ_i = sum_j dS_ij k_j over the key
+ * tiles in ascending order in one accumulator (3 extra GEMMs per tile pair,
+ * ~1.4x the backward flops), and every KV-stationary item sweeps the query
+ * tiles from tile 0 whatever CTA runs it.  Ulysses: dq, dk, dv are then
+ * bitwise reproducible and bitwise identical for every P (the same per-head
+ * arithmetic in the same order).  LSS: bitwise reproducible for a given P
+ * (its dK, dV are sums of P per-rank partials, so they depend on P).
+ * Host-only setting, effective from the next call; every rank should set the
+ * same value (the P-way identity needs it on all ranks). */
+ua_status ua_ctx_set_deterministic(ua_ctx* ctx, int enable);
+ua_status ua_ctx_get_deterministic(const ua_ctx* ctx, int* enable);
 ua_status ua_ctx_phase_times(ua_ctx* ctx, double* ms, int64_t* launches);
 
 /* ------------------------------------------------------------- forward

@@ -29,6 +29,7 @@ STATUS = {0: "UA_OK", 1: "UA_ERR_INVALID_ARG", 2: "UA_ERR_HEAD_DIVISIBILITY", 3:
 EXPORTS = ("ua_version", "ua_status_string", "ua_last_error", "ua_validate", "ua_workspace_size",
            "ua_get_unique_id", "ua_ctx_create", "ua_ctx_destroy", "ua_ctx_comm_stats",
            "ua_ctx_enable_timing", "ua_ctx_phase_times", "ua_ctx_set_a2a_mode", "ua_ctx_get_a2a_mode",
+           "ua_ctx_set_deterministic", "ua_ctx_get_deterministic",
            "ua_ulysses_attn_fwd", "ua_ulysses_attn_bwd", "ua_attn_fwd_segment", "ua_lse_merge",
            "ua_f32_to_bf16_bnhd", "ua_lss_validate", "ua_lss_workspace_size", "ua_lss_attn_fwd", "ua_lss_attn_bwd",
            "ua_layer_sizes", "ua_layer_fwd", "ua_layer_bwd")
@@ -76,6 +77,8 @@ def lib():
         L.ua_ctx_enable_timing.argtypes = [vp, i32]
         L.ua_ctx_set_a2a_mode.argtypes = [vp, i32]
         L.ua_ctx_get_a2a_mode.argtypes = [vp, ctypes.POINTER(i32)]
+        L.ua_ctx_set_deterministic.argtypes = [vp, i32]
+        L.ua_ctx_get_deterministic.argtypes = [vp, ctypes.POINTER(i32)]
         L.ua_ctx_phase_times.argtypes = [vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i64)]
         L.ua_ulysses_attn_fwd.argtypes = [vp, vp, vp, vp, vp, vp, i64, i64, i32, i32, i32, vp, sz, vp]
         L.ua_ulysses_attn_bwd.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, i64, i64, i32, i32, i32, vp, sz, vp]
@@ -190,6 +193,16 @@ class Context:
         m = ctypes.c_int(0)
         _check(lib().ua_ctx_get_a2a_mode(self._h, ctypes.byref(m)))
         return {v: k for k, v in self.A2A_MODES.items()}[m.value]
+
+    def set_deterministic(self, on: bool = True):
+        """Bitwise-reproducible backward: query-stationary dQ kernel instead of
+        the fp32 reduce-add of key-tile partials (ua_ctx_set_deterministic)."""
+        _check(lib().ua_ctx_set_deterministic(self._h, 1 if on else 0))
+
+    def deterministic(self) -> bool:
+        m = ctypes.c_int(0)
+        _check(lib().ua_ctx_get_deterministic(self._h, ctypes.byref(m)))
+        return bool(m.value)
 
     def enable_timing(self, on: bool = True):
         _check(lib().ua_ctx_enable_timing(self._h, 1 if on else 0))

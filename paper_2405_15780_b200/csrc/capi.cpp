@@ -257,7 +257,7 @@ ua_status launch_attention_fwd(const void* q, const void* k, const void* v, int6
 ua_status launch_attention_bwd(Rows q, const void* dout, const void* k, const void* v, Rows kv, ua::ViewArg dk,
                                ua::ViewArg dv, int kv_f32, float* dq_acc, const float* lse, int64_t l_sh,
                                int64_t l_sb, const float* delta, int64_t d_sn, int64_t d_sh, int64_t d_sb, int64_t B,
-                               int heads, int D, float2* lsed, cudaStream_t stream,
+                               int heads, int D, float2* lsed, int deterministic, cudaStream_t stream,
                                const ua::PeerOut* dk_peer = nullptr, const ua::PeerOut* dv_peer = nullptr) {
   ua::BwdParams p;
   std::memset(&p, 0, sizeof(p));
@@ -291,6 +291,7 @@ ua_status launch_attention_bwd(Rows q, const void* dout, const void* k, const vo
   p.scale = float(1.0 / std::sqrt(double(D)));
   p.scale_log2 = float(1.4426950408889634 / std::sqrt(double(D)));
   p.d_io = D;
+  p.deterministic = deterministic;
   UA_CUDA(ua::launch_attn_bwd(p, D, int(B), heads, stream));
   return UA_OK;
 }
@@ -300,11 +301,11 @@ ua_status launch_attention_bwd(const void* q, const void* k, const void* v, cons
                                int64_t sb, ua::ViewArg dk, ua::ViewArg dv, float* dq_acc, const float* lse,
                                int64_t l_sh, int64_t l_sb, const float* delta, int64_t d_sn, int64_t d_sh,
                                int64_t d_sb, int64_t B, int64_t N, int heads, int D, float2* lsed,
-                               cudaStream_t stream, const ua::PeerOut* dk_peer = nullptr,
+                               int deterministic, cudaStream_t stream, const ua::PeerOut* dk_peer = nullptr,
                                const ua::PeerOut* dv_peer = nullptr) {
   const Rows r{q, sn, sh, sb, N};
   return launch_attention_bwd(r, dout, k, v, r, dk, dv, 0, dq_acc, lse, l_sh, l_sb, delta, d_sn, d_sh, d_sb, B, heads,
-                              D, lsed, stream, dk_peer, dv_peer);
+                              D, lsed, deterministic, stream, dk_peer, dv_peer);
 }
 
 // ------------------------------------------------------------ peer all-to-all
@@ -466,6 +467,18 @@ ua_status ua_ctx_set_a2a_mode(ua_ctx* ctx, int mode) {
     }
   }
   ctx->a2a_mode = mode;
+  return UA_OK;
+}
+
+ua_status ua_ctx_set_deterministic(ua_ctx* ctx, int enable) {
+  if (!ctx) return fail(UA_ERR_INVALID_ARG, "ctx is NULL");
+  ctx->deterministic = enable ? 1 : 0;
+  return UA_OK;
+}
+
+ua_status ua_ctx_get_deterministic(const ua_ctx* ctx, int* enable) {
+  if (!ctx || !enable) return fail(UA_ERR_INVALID_ARG, "null argument");
+  *enable = ctx->deterministic;
   return UA_OK;
 }
 
@@ -644,7 +657,7 @@ ua_status ua_ulysses_attn_bwd(ua_ctx* ctx, const void* q, const void* k, const v
       UA_CUDA(cudaMemsetAsync(dq_acc, 0, size_t(B * H * n_pad * D) * 4, stream));
       UA_TRY(launch_attention_bwd(q, k, v, dout, sn, sh, sb, vdk, vdv, dq_acc, lse, N, int64_t(H) * N, delta,
                                   B * int64_t(H), 1, H, B, N, H, D, reinterpret_cast<float2*>(ws + plan.lsed),
-                                  stream));
+                                  ctx->deterministic, stream));
     }
     {
       Phase ph(ctx, UA_PHASE_DQ_FINALIZE, stream);
@@ -694,7 +707,7 @@ ua_status ua_ulysses_attn_bwd(ua_ctx* ctx, const void* q, const void* k, const v
       ua::ViewArg none{nullptr, 0, 0, 0};
       UA_TRY(launch_attention_bwd(rin, rin + S, rin + 2 * S, rin + 3 * S, sn, sh, sb, none, none, dq_acc, lse, N,
                                   int64_t(s.Hl) * N, rdelta, B * int64_t(s.Hl), 1, s.Hl, B, N, s.Hl, D,
-                                  reinterpret_cast<float2*>(ws + plan.lsed), stream, &pdk, &pdv));
+                                  reinterpret_cast<float2*>(ws + plan.lsed), ctx->deterministic, stream, &pdk, &pdv));
     }
     {  // 4. dq = bf16(scale * dq_acc) into the token owners' buffers, then flag
       Phase ph(ctx, UA_PHASE_DQ_FINALIZE, stream);
@@ -746,7 +759,7 @@ ua_status ua_ulysses_attn_bwd(ua_ctx* ctx, const void* q, const void* k, const v
     UA_CUDA(cudaMemsetAsync(dq_acc, 0, size_t(B * s.Hl * n_pad * D) * 4, stream));
     UA_TRY(launch_attention_bwd(recv[0], recv[1], recv[2], recv[3], sn, sh, sb, vdk, vdv, dq_acc, lse, N,
                                 int64_t(s.Hl) * N, recv_delta, B * int64_t(s.Hl), 1, s.Hl, B, N, s.Hl, D,
-                                reinterpret_cast<float2*>(ws + plan.lsed), stream));
+                                reinterpret_cast<float2*>(ws + plan.lsed), ctx->deterministic, stream));
   }
   {
     Phase ph(ctx, UA_PHASE_DQ_FINALIZE, stream);
@@ -895,7 +908,7 @@ ua_status ua_lss_attn_bwd(ua_ctx* ctx, const void* q, const void* k, const void*
     ua::ViewArg vdk{part, ksn, ksh, ksb}, vdv{part + PE, ksn, ksh, ksb};
     UA_TRY(launch_attention_bwd(qr, dout, ws + plan.kv_full, ws + plan.kv_full + S * P, kvr, vdk, vdv, 1, dq_acc, lse,
                                 Nl, int64_t(H) * Nl, delta, B * int64_t(H), 1, H, B, H, D,
-                                reinterpret_cast<float2*>(ws + plan.lsed), stream));
+                                reinterpret_cast<float2*>(ws + plan.lsed), ctx->deterministic, stream));
   }
   {
     Phase ph(ctx, UA_PHASE_DQ_FINALIZE, stream);

@@ -31,6 +31,7 @@ struct ua_ctx {
   // NVLink peer-store all-to-all (UA_A2A_PEER): library-owned buffers, CUDA IPC
   // mapped on every rank (peer[k] = rank k's copy, peer[rank] = local).
   int a2a_mode = UA_A2A_NCCL;
+  int deterministic = 0;  // ua_ctx_set_deterministic: query-stationary dQ, no cross-CTA reduction
   struct PeerBuf {
     void* local = nullptr;
     size_t bytes = 0;

@@ -70,9 +70,12 @@ struct BwdWsCfg {
   static_assert(kSmemBytes <= 232448, "smem budget");
 };
 
-template <int D>
+// kDq = false (deterministic mode): dK, dV only; dQ comes from the query-stationary
+// attn_bwd_dq_kernel (attn_bwd_dq.cu), so no dS^T staging, dQ GEMM or reduction here.
+template <int D, bool kDq>
 __global__ void __launch_bounds__(512, 1) attn_bwd_ws_kernel(const __grid_constant__ BwdParams p) {
   using C = BwdWsCfg<D>;
+  constexpr bool kAlias = C::kAliasDq && kDq;   // dQ shares TMEM with dP^T (D = 128)
   using G = TileGeom<D>;
   constexpr int kSl = C::kSlots;
   extern __shared__ uint8_t smem_raw[];
@@ -104,7 +107,9 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_ws_kernel(const __grid_consta
   const int n_pad = n_q * 128;
   const int n_kt = (p.n_kv + 127) / 128;
   const int n_items = p.batch * p.heads * n_kt;
-  const int start = int((int64_t(blockIdx.x) * C::kStagger) / gridDim.x) % n_q;
+  // Deterministic mode (no dQ reduction to spread out): every item sweeps from
+  // tile 0, so the dK / dV summation order does not depend on the grid (P-invariant).
+  const int start = kDq ? int((int64_t(blockIdx.x) * C::kStagger) / gridDim.x) % n_q : 0;
   auto qslot = [&](int s) { return sSlots + s * C::kSlotBytes; };
   auto doslot = [&](int s) { return sSlots + s * C::kSlotBytes + C::kHalfBytes; };
 
@@ -215,10 +220,10 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_ws_kernel(const __grid_consta
         // first tile of the item
         wait_slot(2 * T);
         issue_s(T, 0);
-        if constexpr (!C::kAliasDq) issue_dp(T, 0);
+        if constexpr (!kAlias) issue_dp(T, 0);
         wait_slot(2 * T + 1);
         issue_s(T, 1);
-        if constexpr (C::kAliasDq) {
+        if constexpr (kAlias) {
           if (T > 0) {
             mbar_wait(dq_empty, (T - 1) & 1);
             tc_fence_after();
@@ -249,7 +254,7 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_ws_kernel(const __grid_consta
                      idesc_g, (acc || kk > 0) ? 1u : 0u);
             mma_commit(&slot_empty[U % kSl]);
             UA_TEV(1, T, 3 + 4 * hh);
-            if (hh == 1) {  // dQ(T) = dS K
+            if (kDq && hh == 1) {  // dQ(T) = dS K
               if (!C::kAliasDq && T > 0) {
                 UA_TEV(1, T, 9);
                 mbar_wait(dq_empty, (T - 1) & 1);
@@ -268,7 +273,7 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_ws_kernel(const __grid_consta
             if (t + 1 < n_q) {  // next tile, this half
               wait_slot(2 * (T + 1) + hh);
               issue_s(T + 1, hh);
-              if constexpr (!C::kAliasDq) {
+              if constexpr (!kAlias) {
                 issue_dp(T + 1, hh);
               } else if (hh == 1) {  // dP^T of the next tile overwrites the dQ region
                 mbar_wait(dq_empty, T & 1);
@@ -326,7 +331,7 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_ws_kernel(const __grid_consta
         const int U = 2 * T + hh, s = U % kSl;
         if (j == 0) UA_TEV(2 + hh, T, 1);
         mbar_wait(&slot_full[s], (U / kSl) & 1);  // (lse, Delta) of this half landed
-        if (T >= C::kNumDs) mbar_wait(&ds_free[T % C::kNumDs], ((T / C::kNumDs) & 1) ^ 1);
+        if (kDq && T >= C::kNumDs) mbar_wait(&ds_free[T % C::kNumDs], ((T / C::kNumDs) & 1) ^ 1);
         mbar_wait(&sdp_full[hh], T & 1);
         if (j == 0) UA_TEV(2 + hh, T, 2);
         tc_fence_after();
@@ -370,7 +375,7 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_ws_kernel(const __grid_consta
           tmem_st8(t_lane + colS + cc / 2, pk_p);
           tmem_st8(t_lane + colDP + cc / 2, pk_ds);
 #pragma unroll
-          for (int qd = 0; qd < 2; ++qd) {
+          for (int qd = 0; qd < 2 * int(kDq); ++qd) {
             const int chunk = ((cc / 8) + qd) ^ (j & 7);
             sts128(atom + chunk * 16, pk_ds[4 * qd], pk_ds[4 * qd + 1], pk_ds[4 * qd + 2], pk_ds[4 * qd + 3]);
           }
@@ -431,7 +436,7 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_ws_kernel(const __grid_consta
       tc_fence_before();
       mbar_arrive(acc_free);
     }
-  } else if (warp >= 12) {
+  } else if (kDq && warp >= 12) {
     // ------------------------------------------------------------ dQ drain
     const int quad = warp % 4;
     const int r = quad * 32 + lane;  // query row within the tile
@@ -501,7 +506,7 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_ws_kernel(const __grid_consta
   if (warp == 1) tmem_free<512>(tbase);
 }
 
-template <int D>
+template <int D, bool kDq>
 cudaError_t launch_bwd_ws_impl(const BwdParams& p, cudaStream_t stream) {
   using C = BwdWsCfg<D>;
   static int num_sms = 0;
@@ -510,7 +515,7 @@ cudaError_t launch_bwd_ws_impl(const BwdParams& p, cudaStream_t stream) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
     cudaError_t e =
-        cudaFuncSetAttribute(attn_bwd_ws_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+        cudaFuncSetAttribute(attn_bwd_ws_kernel<D, kDq>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
     if (e != cudaSuccess) return e;
   }
   const int64_t items = int64_t(p.batch) * p.heads * ((p.n_kv + 127) / 128);
@@ -518,7 +523,7 @@ cudaError_t launch_bwd_ws_impl(const BwdParams& p, cudaStream_t stream) {
 #if UA_TRACE
   trace_reset();
 #endif
-  attn_bwd_ws_kernel<D><<<grid, C::kThreads, C::kSmemBytes, stream>>>(p);
+  attn_bwd_ws_kernel<D, kDq><<<grid, C::kThreads, C::kSmemBytes, stream>>>(p);
 #if UA_TRACE
   trace_dump("bwd");
 #endif
@@ -528,11 +533,23 @@ cudaError_t launch_bwd_ws_impl(const BwdParams& p, cudaStream_t stream) {
 }  // namespace
 
 cudaError_t launch_attn_bwd_ws(const BwdParams& p, int D, cudaStream_t stream) {
+  if (p.deterministic) {  // dK, dV here; dQ by the query-stationary kernel (no cross-CTA reduction)
+    cudaError_t e = cudaSuccess;
+    switch (D) {
+      case 32: e = launch_bwd_ws_impl<32, false>(p, stream); break;
+      case 64: e = launch_bwd_ws_impl<64, false>(p, stream); break;
+      case 72: e = launch_bwd_ws_impl<80, false>(p, stream); break;
+      case 128: e = launch_bwd_ws_impl<128, false>(p, stream); break;
+      default: return cudaErrorInvalidValue;
+    }
+    if (e != cudaSuccess) return e;
+    return launch_attn_bwd_dq(p, D, stream);
+  }
   switch (D) {
-    case 32: return launch_bwd_ws_impl<32>(p, stream);
-    case 64: return launch_bwd_ws_impl<64>(p, stream);
-    case 72: return launch_bwd_ws_impl<80>(p, stream);   // padded MMA head dim, p.d_io = 72
-    case 128: return launch_bwd_ws_impl<128>(p, stream);
+    case 32: return launch_bwd_ws_impl<32, true>(p, stream);
+    case 64: return launch_bwd_ws_impl<64, true>(p, stream);
+    case 72: return launch_bwd_ws_impl<80, true>(p, stream);   // padded MMA head dim, p.d_io = 72
+    case 128: return launch_bwd_ws_impl<128, true>(p, stream);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -75,6 +75,7 @@ struct alignas(64) BwdParams {
   float scale;        // 1/sqrt(D)
   float scale_log2;   // log2(e)/sqrt(D)
   int d_io;           // head dim of the I/O tensors and of dq_acc rows (72 runs in the D = 80 kernel)
+  int deterministic;  // 1: dQ by the query-stationary kernel, stored (not reduce-added) into dq_acc
 };
 
 cudaError_t launch_attn_fwd(const FwdParams& p, int D, int B, int heads, cudaStream_t stream);
@@ -82,6 +83,9 @@ cudaError_t launch_attn_fwd(const FwdParams& p, int D, int B, int heads, cudaStr
 cudaError_t launch_attn_fwd_split(const FwdParams& p, int D, int B, int heads, cudaStream_t stream);
 cudaError_t launch_attn_bwd(const BwdParams& p, int D, int B, int heads, cudaStream_t stream);
 cudaError_t launch_attn_bwd_ws(const BwdParams& p, int D, cudaStream_t stream);
+// Deterministic dQ (attn_bwd_dq.cu): query-stationary, dq_acc rows = sum_j dS_ij k_j (unscaled, fp32,
+// plain stores, fixed key order).  Called by launch_attn_bwd_ws when p.deterministic.
+cudaError_t launch_attn_bwd_dq(const BwdParams& p, int D, cudaStream_t stream);
 
 // ---- layout / elementwise kernels (layout.cu) --------------------------------
 // Sequence shard -> per-destination send chunks, for `ntensors` tensors:

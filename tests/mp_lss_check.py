@@ -35,6 +35,7 @@ def main():
     ap.add_argument("--H", type=int, default=8)
     ap.add_argument("--D", type=int, default=64)
     ap.add_argument("--sigma", type=float, default=1.0)
+    ap.add_argument("--det", type=int, default=0, help="deterministic backward: dq also bitwise reproducible")
     a = ap.parse_args()
     rank, P = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
@@ -48,6 +49,7 @@ def main():
     qs, ks, vs, ds = (t[:, sl].contiguous().to(dev) for t in (q, k, v, do))
 
     ctx = ua.Context(P=P, rank=rank, device=local)
+    ctx.set_deterministic(bool(a.det))
     c0, b0 = ctx.comm_stats()
     r = ua.lss_attn_fwd(ctx, qs, ks, vs)
     c1, b1 = ctx.comm_stats()
@@ -65,6 +67,8 @@ def main():
     torch.cuda.synchronize()
     assert torch.equal(r2.out, r.out) and torch.equal(r2.lse, r.lse)
     assert torch.equal(dk2, dk) and torch.equal(dv2, dv)
+    if a.det:
+        assert torch.equal(dq2, dq)
 
     def gather(t):
         parts = [torch.empty_like(t) for _ in range(P)]

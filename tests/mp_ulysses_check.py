@@ -32,6 +32,7 @@ def main():
     ap.add_argument("--D", type=int, default=64)
     ap.add_argument("--sigma", type=float, default=1.0)
     ap.add_argument("--mode", default="nccl", choices=["nccl", "peer"])
+    ap.add_argument("--det", type=int, default=0, help="deterministic backward: P-way grads == P=1 grads bitwise")
     a = ap.parse_args()
     rank, P = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
@@ -47,6 +48,7 @@ def main():
     ctx = ua.Context(P=P, rank=rank, device=local)
     ctx.set_a2a_mode(a.mode)
     assert ctx.a2a_mode() == a.mode
+    ctx.set_deterministic(bool(a.det))
     # head limit: every rank must get the same error, before any collective
     try:
         ua.ulysses_attn_fwd(ctx, *(torch.zeros(1, 4, 1, D, dtype=torch.bfloat16, device=dev) for _ in range(3)))
@@ -73,6 +75,8 @@ def main():
     assert torch.equal(r2.out, r.out) and torch.equal(r2.lse, r.lse)
     assert torch.equal(dk2, dk) and torch.equal(dv2, dv)
     assert (dq2.float() - dq.float()).abs().max().item() <= 2e-2
+    if a.det:
+        assert torch.equal(dq2, dq)
 
     def gather(t):
         parts = [torch.empty_like(t) for _ in range(P)]
@@ -86,13 +90,17 @@ def main():
         dq_g, dk_g, dv_g = (torch.cat(x, 1).float().cpu().numpy() for x in (dqs, dks, dvs))
         # P=1 on the same inputs, same device: bitwise forward equality
         c1ctx = ua.Context(P=1, device=local)
+        c1ctx.set_deterministic(bool(a.det))
         r1 = ua.ulysses_attn_fwd(c1ctx, q.to(dev), k.to(dev), v.to(dev))
         g1 = ua.ulysses_attn_bwd(c1ctx, q.to(dev), k.to(dev), v.to(dev), r1.out, r1.lse, do.to(dev))
         torch.cuda.synchronize()
         assert np.array_equal(out_g, r1.out.float().cpu().numpy()), "P-way forward != P=1 forward"
         assert np.array_equal(lse_g, r1.lse.cpu().numpy()), "P-way lse != P=1 lse"
         for x, y in zip((dq_g, dk_g, dv_g), g1):
-            assert np.abs(x - y.float().cpu().numpy()).max() <= 2e-2
+            if a.det:   # same per-head arithmetic in a fixed order: bitwise
+                assert np.array_equal(x, y.float().cpu().numpy()), "P-way grads != P=1 grads (deterministic)"
+            else:
+                assert np.abs(x - y.float().cpu().numpy()).max() <= 2e-2
         f64 = [synth.to_f64(t) for t in (q, k, v, do)]
         ref, ref_lse, absv = oracle.attn_fwd(*f64[:3], with_abs=True)
         gate_out(out_g, ref, gate_a=a.sigma == 1.0, absv=absv)

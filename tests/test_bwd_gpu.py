@@ -105,3 +105,64 @@ def test_bwd_deterministic_dkdv(ua, ctx):
     a = run_fwd_bwd(ua, ctx, q, k, v, do)
     b = run_fwd_bwd(ua, ctx, q, k, v, do)
     assert np.array_equal(a[1], b[1]) and np.array_equal(a[2], b[2])
+
+
+# ------------------------------------------------------------ deterministic mode
+@pytest.fixture(scope="module")
+def dctx(ua):
+    c = ua.Context(P=1)
+    c.set_deterministic(True)
+    assert c.deterministic()
+    yield c
+    c.close()
+
+
+@pytest.mark.parametrize("B,N,H,D,sigma", [
+    (1, 256, 4, 32, 1.0),      # c1
+    (1, 2, 2, 64, 1.0),        # two tokens
+    (1, 129, 2, 64, 2.0),      # ragged query and key tails
+    (1, 1000, 2, 128, 2.0),
+    (1, 4050, 2, 64, 1.0),
+    (2, 384, 2, 64, 1.0),      # B > 1
+    (1, 1000, 3, 72, 2.0),     # D = 72 (padded 80-wide tiles)
+])
+def test_bwd_deterministic_parity(ua, dctx, B, N, H, D, sigma):
+    """Query-stationary dQ + dQ-less KV-stationary kernel against the fp64 oracle."""
+    check(ua, dctx, B, N, H, D, sigma, seed=300 + N)
+
+
+def test_bwd_deterministic_one_token(ua, dctx):
+    """N = 1: dV = dO, dQ = dK = 0.  dQ is dS k with dS = dP - Delta, two
+    fp32 sums of the same D products in different orders, so it is zero only up
+    to fp32 rounding (the relative gate is undefined for an all-zero reference)."""
+    q, k, v, do = synth.qkv(1, 1, 2, 64, seed=3, with_do=True)
+    dq, dk, dv = run_fwd_bwd(ua, dctx, q, k, v, do)
+    assert np.abs(dq).max() <= 1e-4 and np.abs(dk).max() <= 1e-4
+    assert np.array_equal(dv, do.float().numpy())
+
+
+@pytest.mark.parametrize("N,H,D", [(2048, 2, 64), (1000, 2, 128), (777, 2, 32)])
+def test_bwd_deterministic_bitwise(ua, ctx, dctx, N, H, D):
+    """Deterministic mode: dq, dk, dv bitwise equal run to run, and within
+    bf16 rounding of the default mode's (which sums the same per-tile partials
+    in another order: staggered query sweeps, concurrent dQ reduce-adds)."""
+    q, k, v, do = synth.qkv(1, N, H, D, seed=21, with_do=True)
+    a = run_fwd_bwd(ua, dctx, q, k, v, do)
+    b = run_fwd_bwd(ua, dctx, q, k, v, do)
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
+    ref = run_fwd_bwd(ua, ctx, q, k, v, do)
+    for x, y in zip(a, ref):
+        assert np.abs(x - y).max() <= 2 ** -7 * np.abs(y).max() + 1e-6
+
+
+def test_bwd_deterministic_c2(ua, dctx):
+    """c2 (N=8192, H=16, D=64) in deterministic mode: oracle on 4 of the 16 heads."""
+    B, N, H, D = 1, 8192, 16, 64
+    q, k, v, do = synth.qkv(B, N, H, D, seed=synth.BASE_SEED, with_do=True)
+    got = run_fwd_bwd(ua, dctx, q, k, v, do)
+    heads = [0, 7, 15]
+    sub = [synth.to_f64(t)[:, :, heads] for t in (q, k, v, do)]
+    dq, dk, dv, _, _, gabs = oracle.attn_bwd(*sub, with_abs=True)
+    for g, ref, a in zip(got, (dq, dk, dv), gabs):
+        gate_grad(g[:, :, heads], ref, gate_a=True, gabs=a)

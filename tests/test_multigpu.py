@@ -42,6 +42,23 @@ def test_ulysses_p_way(P, N, H, D, sigma, mode):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["nccl", "peer"])
+@pytest.mark.parametrize("P,N,H,D,sigma", [
+    (2, 4096, 8, 64, 1.0),
+    (2, 2050, 4, 128, 2.0),     # ragged: N/P = 1025
+    (4, 4096, 8, 32, 2.0),
+    (8, 8192, 16, 64, 1.0),
+])
+def test_ulysses_p_way_deterministic(P, N, H, D, sigma, mode):
+    """Deterministic backward: P-way dq, dk, dv bitwise equal to P = 1."""
+    if torch.cuda.device_count() < P:
+        pytest.skip(f"needs {P} GPUs")
+    r = torchrun(P, os.path.join(ROOT, "tests", "mp_ulysses_check.py"), f"--N={N}", f"--H={H}", f"--D={D}",
+                 f"--sigma={sigma}", f"--mode={mode}", "--det=1")
+    assert r.returncode == 0 and "MP_OK" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("P,B,N,H,D,sigma", [
     (2, 1, 4096, 8, 64, 1.0),
     (2, 1, 2048, 4, 128, 2.0),
@@ -57,6 +74,17 @@ def test_lss_p_way(P, B, N, H, D, sigma):
         pytest.skip(f"needs {P} GPUs")
     r = torchrun(P, os.path.join(ROOT, "tests", "mp_lss_check.py"), f"--B={B}", f"--N={N}", f"--H={H}", f"--D={D}",
                  f"--sigma={sigma}")
+    assert r.returncode == 0 and "LSS_OK" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("P,B,N,H,D", [(2, 1, 4096, 8, 64), (4, 2, 2048, 2, 128)])
+def test_lss_p_way_deterministic(P, B, N, H, D):
+    """LSS with the deterministic backward: oracle gates, dq bitwise run to run."""
+    if torch.cuda.device_count() < P:
+        pytest.skip(f"needs {P} GPUs")
+    r = torchrun(P, os.path.join(ROOT, "tests", "mp_lss_check.py"), f"--B={B}", f"--N={N}", f"--H={H}", f"--D={D}",
+                 "--sigma=1.0", "--det=1")
     assert r.returncode == 0 and "LSS_OK" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
 
 
