@@ -36,6 +36,12 @@
 #ifndef UA_BWD_KV_TMEM
 #define UA_BWD_KV_TMEM 1    // D <= 64: K, V copied into TMEM once per work item (TS MMAs)
 #endif
+#ifndef UA_BWD_SEP_P
+#define UA_BWD_SEP_P 1      // dQ-less variant: separate TMEM P^T, next S^T under the exponentials
+#endif
+#ifndef UA_BWD_SEP_POLY_MOD
+#define UA_BWD_SEP_POLY_MOD 0   // same as UA_BWD_POLY_MOD for the separate-P^T variant (A/B: none is best)
+#endif
 #ifndef UA_BWD_STAGGER
 #define UA_BWD_STAGGER 16   // query-tile window the persistent CTAs' start tiles are spread over
 #endif
@@ -66,16 +72,30 @@ struct BwdWsCfg {
   static constexpr int kLsedBytes = 128 * 4;                   // per slot: 64 x -lse*log2e, 64 x -Delta
   static constexpr bool kPolyExp = UA_BWD_POLY_MOD > 0;
   static constexpr int kSmemBytes = 1024 + 2 * G::kTileBytes + kSlots * kSlotBytes + kNumDs * kDsBytes +
-                                    kStageBoxes * kBoxBytes + kSlots * kLsedBytes + 256;
+                                    kStageBoxes * kBoxBytes + kSlots * kLsedBytes + 512;
+  // Without the dQ GEMM (deterministic mode) the dQ columns hold a separate bf16
+  // P^T per half (32 columns each), so the next S^T GEMM can overwrite S^T as
+  // soon as the elementwise warps have loaded it (D = 128 has no dQ columns).
+  static constexpr uint32_t kColP = (kKvTmem && kColV + D / 2 + 64 <= 512) ? kColV + D / 2 : kColDQ;
+  static constexpr bool kSepPFits = !kAliasDq && (kColP == kColDQ ? (kKvTmem ? kColK : 512u) : 512u) >= kColP + 64;
   static_assert(kSmemBytes <= 232448, "smem budget");
 };
+
+// Separate-P^T pipeline of the dQ-less variant (needs 64 spare TMEM columns).
+template <int D, bool kDq>
+__host__ __device__ constexpr bool ws_sep_p() { return !kDq && BwdWsCfg<D>::kSepPFits && UA_BWD_SEP_P; }
+// kSepP: 20 warps -- each 64-query half has two elementwise warpgroups of 32 query columns.
+template <int D, bool kDq>
+__host__ __device__ constexpr int ws_threads() { return ws_sep_p<D, kDq>() ? 640 : 512; }
 
 // kDq = false (deterministic mode): dK, dV only; dQ comes from the query-stationary
 // attn_bwd_dq_kernel (attn_bwd_dq.cu), so no dS^T staging, dQ GEMM or reduction here.
 template <int D, bool kDq>
-__global__ void __launch_bounds__(512, 1) attn_bwd_ws_kernel(const __grid_constant__ BwdParams p) {
+__global__ void __launch_bounds__(ws_threads<D, kDq>(), 1) attn_bwd_ws_kernel(const __grid_constant__ BwdParams p) {
   using C = BwdWsCfg<D>;
   constexpr bool kAlias = C::kAliasDq && kDq;   // dQ shares TMEM with dP^T (D = 128)
+  constexpr bool kSepP = ws_sep_p<D, kDq>();
+  constexpr int kEwArrive = kSepP ? 256 : 128;   // arrivals per half on s_loaded / p_ready / ds_ready
   using G = TileGeom<D>;
   constexpr int kSl = C::kSlots;
   extern __shared__ uint8_t smem_raw[];
@@ -99,7 +119,11 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_ws_kernel(const __grid_consta
   uint64_t* slot_full = bars + 12;    // [kSl]
   uint64_t* slot_empty = slot_full + kSl;
   uint64_t* kv_tmem = slot_empty + kSl;  // K, V copied into TMEM for this item
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(kv_tmem + 1);
+  uint64_t* dp_full = kv_tmem + 1;    // [2] kSepP: dP^T[h] computed (sdp_full then signals S^T alone)
+  uint64_t* s_loaded = dp_full + 2;   // [2] kSepP: S^T[h] in registers, may be overwritten
+  uint64_t* p_ready = s_loaded + 2;   // [2] kSepP: P^T[h] stored
+  uint64_t* p_free = p_ready + 2;     // [2] kSepP: dV GEMM has read P^T[h]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(p_free + 2);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -123,7 +147,11 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_ws_kernel(const __grid_consta
     mbar_init(kv_tmem, 128);
     for (int h = 0; h < 2; ++h) {
       mbar_init(&sdp_full[h], 1);
-      mbar_init(&ds_ready[h], 128);
+      mbar_init(&ds_ready[h], kEwArrive);
+      mbar_init(&dp_full[h], 1);
+      mbar_init(&s_loaded[h], kEwArrive);
+      mbar_init(&p_ready[h], kEwArrive);
+      mbar_init(&p_free[h], 1);
     }
     for (int i = 0; i < C::kNumDs; ++i) mbar_init(&ds_free[i], 1);
     for (int s = 0; s < kSl; ++s) {
@@ -138,8 +166,16 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_ws_kernel(const __grid_consta
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
 
+  // kSepP: 640 threads launch with 96 registers each; the producer / MMA
+  // warpgroup gives 40 of them to the four elementwise warpgroups (56 + 4 x 104
+  // <= 5 x 96: setmaxnreg.inc can only take what the CTA's own warps released).
+  // Each role branch re-balances first thing so ptxas sees which limit applies.
+#define UA_BWD_REGS_LOW() do { if constexpr (kSepP) setmaxnreg_dec<56>(); } while (0)
+#define UA_BWD_REGS_HIGH() do { if constexpr (kSepP) setmaxnreg_inc<104>(); } while (0)
+
   if (warp == 0) {
     // ------------------------------------------------------------ producer
+    UA_BWD_REGS_LOW();
     if (lane == 0) {
       tma_prefetch_desc(&p.tm_qh);
       tma_prefetch_desc(&p.tm_k);
@@ -179,6 +215,7 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_ws_kernel(const __grid_consta
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
+    UA_BWD_REGS_LOW();
     if (elect_one()) {
       const uint32_t idesc_s = idesc_bf16_f32(128, 64, false, false);  // S^T, dP^T half: N = 64 queries
       const uint32_t idesc_g = idesc_bf16_f32(128, D, false, true);    // dV, dK: A = TMEM, B MN-major
@@ -213,6 +250,73 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_ws_kernel(const __grid_consta
         }
         mma_commit(&sdp_full[hh]);
       };
+      if constexpr (kSepP) {
+        // S^T(T+1) right after the elementwise warps have loaded S^T(T); dV(T)
+        // once P^T(T) is stored; dK(T) and then dP^T(T+1) once dS^T(T) is.
+        auto issue_s1 = [&](int T1, int hh) {
+          issue_s(T1, hh);
+          mma_commit(&sdp_full[hh]);
+        };
+        auto issue_dp1 = [&](int T1, int hh) {
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk) {
+            if constexpr (C::kKvTmem)
+              mma_ts(tbase + C::kColDP + 64 * hh, tbase + C::kColV + kk * 8,
+                     kmajor_desc_r<D, 64>(do_at(2 * T1 + hh), kk), idesc_s, kk > 0 ? 1u : 0u);
+            else
+              mma_ss(tbase + C::kColDP + 64 * hh, kmajor_desc_r<D, 128>(sVa, kk),
+                     kmajor_desc_r<D, 64>(do_at(2 * T1 + hh), kk), idesc_s, kk > 0 ? 1u : 0u);
+          }
+          mma_commit(&dp_full[hh]);
+        };
+        int T = 0, it = 0;
+        for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
+          mbar_wait(C::kKvTmem ? kv_tmem : kv_full, it & 1);
+          tc_fence_after();
+          for (int hh = 0; hh < 2; ++hh) {
+            wait_slot(2 * T + hh);
+            issue_s1(T, hh);
+            issue_dp1(T, hh);
+          }
+          if (it > 0) {
+            mbar_wait(acc_free, (it - 1) & 1);  // previous item's dV / dK drained
+            tc_fence_after();
+          }
+          // Fixed issue order (half 0, then half 1, per tile): the dV / dK
+          // summation order must not depend on timing.  (Issuing whichever half
+          // is ready first measured no faster and breaks reproducibility.)
+          for (int t = 0; t < n_q; ++t, ++T) {
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+              const int U = 2 * T + hh;
+              const bool more = t + 1 < n_q;
+              if (more) {
+                mbar_wait(&s_loaded[hh], T & 1);
+                wait_slot(2 * (T + 1) + hh);
+                issue_s1(T + 1, hh);
+              }
+              mbar_wait(&p_ready[hh], T & 1);
+              tc_fence_after();
+              const uint32_t acc = (t > 0 || hh > 0) ? 1u : 0u;
+#pragma unroll
+              for (int kk = 0; kk < 4; ++kk)
+                mma_ts(tbase + C::kColDV, tbase + C::kColP + 32 * hh + kk * 8, mnmajor_desc_r<D, 64>(do_at(U), kk),
+                       idesc_g, (acc || kk > 0) ? 1u : 0u);
+              mma_commit(&p_free[hh]);
+              mbar_wait(&ds_ready[hh], T & 1);
+              tc_fence_after();
+#pragma unroll
+              for (int kk = 0; kk < 4; ++kk)  // dS^T queries [32g, 32g+32) were packed at column 32g
+                mma_ts(tbase + C::kColDK, tbase + C::kColDP + 64 * hh + kk * 8 + (kk >= 2 ? 16 : 0),
+                       mnmajor_desc_r<D, 64>(q_at(U), kk), idesc_g, (acc || kk > 0) ? 1u : 0u);
+              mma_commit(&slot_empty[U % kSl]);
+              if (more) issue_dp1(T + 1, hh);
+            }
+          }
+          mma_commit(acc_full);
+          mma_commit(kv_empty);
+        }
+      } else {
       int T = 0, it = 0;
       for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
         mbar_wait(C::kKvTmem ? kv_tmem : kv_full, it & 1);
@@ -287,15 +391,18 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_ws_kernel(const __grid_consta
         mma_commit(acc_full);
         mma_commit(kv_empty);
       }
+      }  // !kSepP
     }
     __syncwarp();
-  } else if (warp >= 4 && warp < 12) {
+  } else if (warp >= 4 && warp < (kSepP ? 20 : 12)) {
     // ------------------------------------------------------------ elementwise (half hh)
-    const int hh = (warp - 4) / 4;
+    UA_BWD_REGS_HIGH();
+    const int hh = kSepP ? (warp - 4) / 8 : (warp - 4) / 4;
+    const int g = kSepP ? ((warp - 4) / 4) % 2 : 0;   // kSepP: query columns [32g, 32g+32) of the half
     const int quad = warp % 4;
     const int j = quad * 32 + lane;  // key row within the tile
     const uint32_t t_lane = tbase + (uint32_t(quad * 32) << 16);
-    const uint32_t colS = C::kColS + 64 * hh, colDP = C::kColDP + 64 * hh;
+    const uint32_t colS = C::kColS + 64 * hh + 32 * g, colDP = C::kColDP + 64 * hh + 32 * g;
     const float c = p.scale_log2;
     const float2 c2 = make_float2(c, c);
     int T = 0, it = 0;
@@ -303,7 +410,7 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_ws_kernel(const __grid_consta
       const int kt = item % n_kt, bh = item / n_kt;
       const int b = bh / p.heads, h = bh % p.heads;
       if constexpr (C::kKvTmem) {
-        if (hh == 0) {  // copy this item's K, V rows (row j per thread) into TMEM as bf16 pairs
+        if (hh == 0 && g == 0) {  // copy this item's K, V rows (row j per thread) into TMEM as bf16 pairs
           mbar_wait(kv_full, it & 1);
           const uint32_t sw = (uint32_t(j * G::kSw) >> 7) & uint32_t(G::kSw / 16 - 1);
           uint32_t rk[D / 2], rv[D / 2];
@@ -327,6 +434,68 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_ws_kernel(const __grid_consta
           mbar_arrive(kv_tmem);
         }
       }
+      if constexpr (kSepP) {
+        for (int t = 0; t < n_q; ++t, ++T) {
+          const int U = 2 * T + hh, s = U % kSl;
+          mbar_wait(&slot_full[s], (U / kSl) & 1);  // (lse, Delta) of this half landed
+          mbar_wait(&sdp_full[hh], T & 1);          // S^T(T) computed
+          tc_fence_after();
+          const uint32_t nl_s = smem_u32(sLsed + s * 128 + 32 * g);
+          const uint32_t nd_s = nl_s + 64 * 4;
+          uint32_t rs[32];
+          tmem_ld16(t_lane + colS, *reinterpret_cast<uint32_t(*)[16]>(rs));
+          tmem_ld16(t_lane + colS + 16, *reinterpret_cast<uint32_t(*)[16]>(rs + 16));
+          tmem_ld_wait();
+          tc_fence_before();
+          mbar_arrive(&s_loaded[hh]);                  // the next S^T GEMM may overwrite S^T[hh]
+          float pv[32];
+          uint32_t pk_p[16];
+#pragma unroll
+          for (int x = 0; x < 32; x += 4) {
+            const float4 nl = lds128(nl_s + x * 4);
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+              const float2 arg = __ffma2_rn(make_float2(__uint_as_float(rs[x + 2 * u]), __uint_as_float(rs[x + 2 * u + 1])),
+                                            c2, u == 0 ? make_float2(nl.x, nl.y) : make_float2(nl.z, nl.w));
+              const bool poly = UA_BWD_SEP_POLY_MOD > 0 &&
+                                ((x / 2 + u) % (UA_BWD_SEP_POLY_MOD > 0 ? UA_BWD_SEP_POLY_MOD : 1)) == 1;
+              const float2 pp = poly ? exp2_poly2(arg) : make_float2(ex2(arg.x), ex2(arg.y));
+              pv[x + 2 * u] = pp.x;
+              pv[x + 2 * u + 1] = pp.y;
+              pk_p[x / 2 + u] = pack_bf16x2(pp.x, pp.y);
+            }
+          }
+          if (T > 0) mbar_wait(&p_free[hh], (T - 1) & 1);  // dV(T-1) has read P^T[hh]
+          tc_fence_after();
+          tmem_st16(t_lane + C::kColP + 32 * hh + 16 * g, pk_p);
+          tmem_st_wait();
+          tc_fence_before();
+          mbar_arrive(&p_ready[hh]);
+          mbar_wait(&dp_full[hh], T & 1);           // dP^T(T) computed
+          tc_fence_after();
+          uint32_t rdA[16], rdB[16];
+          tmem_ld16(t_lane + colDP, rdA);
+          tmem_ld16(t_lane + colDP + 16, rdB);
+          tmem_ld_wait();
+          uint32_t pk_ds[16];
+#pragma unroll
+          for (int x = 0; x < 32; x += 4) {
+            const uint32_t* rd = x < 16 ? rdA + x : rdB + (x - 16);
+            const float4 nd = lds128(nd_s + x * 4);
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+              const float2 dd = __fadd2_rn(make_float2(__uint_as_float(rd[2 * u]), __uint_as_float(rd[2 * u + 1])),
+                                           u == 0 ? make_float2(nd.x, nd.y) : make_float2(nd.z, nd.w));
+              const float2 ds = __fmul2_rn(make_float2(pv[x + 2 * u], pv[x + 2 * u + 1]), dd);
+              pk_ds[x / 2 + u] = pack_bf16x2(ds.x, ds.y);
+            }
+          }
+          tmem_st16(t_lane + colDP, pk_ds);           // dS^T over this group's dP^T columns (all read)
+          tmem_st_wait();
+          tc_fence_before();
+          mbar_arrive(&ds_ready[hh]);
+        }
+      } else
       for (int t = 0; t < n_q; ++t, ++T) {
         const int U = 2 * T + hh, s = U % kSl;
         if (j == 0) UA_TEV(2 + hh, T, 1);
@@ -388,6 +557,7 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_ws_kernel(const __grid_consta
         mbar_arrive(&ds_ready[hh]);
       }
       // ------------------------------------------------ dV (hh=0) / dK (hh=1) epilogue
+      if (g != 0) continue;  // kSepP: the first warpgroup of each half drains dV / dK
       mbar_wait(acc_full, it & 1);
       tc_fence_after();
       const int krow = kt * 128 + j;
@@ -499,7 +669,11 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_ws_kernel(const __grid_consta
       }
     }
     if (leader) bulk_wait<0>();
+  } else {
+    UA_BWD_REGS_LOW();  // warps 2, 3 (and the idle dQ-drain warpgroup without the dQ GEMM)
   }
+#undef UA_BWD_REGS_LOW
+#undef UA_BWD_REGS_HIGH
 
   tc_fence_before();
   __syncthreads();
@@ -523,7 +697,7 @@ cudaError_t launch_bwd_ws_impl(const BwdParams& p, cudaStream_t stream) {
 #if UA_TRACE
   trace_reset();
 #endif
-  attn_bwd_ws_kernel<D, kDq><<<grid, C::kThreads, C::kSmemBytes, stream>>>(p);
+  attn_bwd_ws_kernel<D, kDq><<<grid, ws_threads<D, kDq>(), C::kSmemBytes, stream>>>(p);
 #if UA_TRACE
   trace_dump("bwd");
 #endif

@@ -19,6 +19,7 @@ ap.add_argument("--H", type=int, default=32)
 ap.add_argument("--D", type=int, default=64)
 ap.add_argument("--what", default="both")
 ap.add_argument("--rounds", type=int, default=6)
+ap.add_argument("--det", action="store_true", help="deterministic backward (ua_ctx_set_deterministic)")
 a = ap.parse_args()
 
 vp, i64, i32, sz = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_size_t
@@ -37,6 +38,9 @@ for path in a.libs:
     L.ua_ulysses_attn_bwd.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, i64, i64, i32, i32, i32, vp, sz, vp]
     h = vp(0)
     assert L.ua_ctx_create(None, 1, 0, torch.cuda.current_device(), ctypes.byref(h)) == 0
+    if a.det:
+        L.ua_ctx_set_deterministic.argtypes = [vp, i32]
+        assert L.ua_ctx_set_deterministic(h, 1) == 0
     fb, bb = sz(0), sz(0)
     L.ua_workspace_size(B, N, H, D, 1, ctypes.byref(fb), ctypes.byref(bb))
     ws = torch.empty(max(fb.value, bb.value, 256), dtype=torch.uint8, device="cuda")

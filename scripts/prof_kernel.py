@@ -16,10 +16,12 @@ ap.add_argument("--H", type=int, default=32)
 ap.add_argument("--D", type=int, default=64)
 ap.add_argument("--iters", type=int, default=2)
 ap.add_argument("--fwd-only", action="store_true")
+ap.add_argument("--det", action="store_true", help="deterministic backward")
 a = ap.parse_args()
 torch.manual_seed(0)
 q, k, v, do = (torch.randn(1, a.N, a.H, a.D, device="cuda").bfloat16() for _ in range(4))
 ctx = ua.Context(P=1)
+ctx.set_deterministic(a.det)
 for _ in range(a.iters):
     r = ua.ulysses_attn_fwd(ctx, q, k, v)
     if not a.fwd_only:
