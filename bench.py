@@ -46,6 +46,9 @@ PAPER_CONTEXT = {
 }
 UNIT = "TFLOP/s"
 WORKLOAD = dict(name="c4", B=1, N=188416, H=32, D=64)
+# BASELINE.json configs by (N, H, D) (c1 is the oracle-sized parity case)
+CONFIG_NAMES = {(256, 4, 32): "c1", (8192, 16, 64): "c2", (65536, 16, 128): "c3", (188416, 32, 64): "c4",
+                (1048576, 32, 128): "c5"}
 
 
 def flops_per_step(B, N, H, D):
@@ -184,6 +187,7 @@ def main():
     ap.add_argument("--N", type=int, default=WORKLOAD["N"])
     ap.add_argument("--H", type=int, default=WORKLOAD["H"])
     ap.add_argument("--D", type=int, default=WORKLOAD["D"])
+    ap.add_argument("--B", type=int, default=WORKLOAD["B"], help="batch (the paper's local batch is 4, P:425)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--a2a", default="nccl", choices=["nccl", "peer"],
                     help="all-to-all transport for P > 1: NCCL send/recv, or NVLink peer stores from the kernels")
@@ -208,7 +212,7 @@ def main():
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    B, N, H, D = WORKLOAD["B"], args.N, args.H, args.D
+    B, N, H, D = args.B, args.N, args.H, args.D
     lss = args.strategy == "lss"
     (ua.lss_validate if lss else ua.validate)(B, N, H, D, P)
     Nl = N // P
@@ -380,7 +384,7 @@ def main():
             "metric": METRIC, "value": tflops, "unit": UNIT, "n_gpus": P, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": f"c4: {'LSS' if lss else 'Ulysses'} attention fwd+bwd, N={N} tokens, H={H}, D={D}, B={B}, P={P}",
+            "config": {"workload": f"{CONFIG_NAMES.get((N, H, D), 'custom')}: {'LSS' if lss else 'Ulysses'} attention fwd+bwd, N={N} tokens, H={H}, D={D}, B={B}, P={P}",
                        "B": B, "N": N, "H": H, "D": D, "P": P, "parallelism": f"{args.strategy}-sp{P}",
                        "a2a": ("nccl all-gather/reduce-scatter" if lss else args.a2a) if P > 1 else "none",
                        "l2": "inputs larger than L2 (each q/k/v/dO shard "
