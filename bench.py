@@ -293,7 +293,8 @@ def main():
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
         try:
-            traffic = None if lss else json.load(open(tp)).get(f"attn_bwd_D{D}_N{N}_P{P}")
+            key = f"attn_bwd{'_det' if args.deterministic else ''}_D{D}_N{N}_P{P}"
+            traffic = None if lss or B != 1 else json.load(open(tp)).get(key)
         except Exception:
             traffic = None
     roofline = {"bound": "tensor", "kernel": "attn_bwd_kernel", "achieved": kb["tflops"],

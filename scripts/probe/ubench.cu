@@ -2,8 +2,10 @@
 // the B200 (calibrates the softmax cost model in DESIGN.md).  Each thread runs
 // 8 independent chains; one CTA per SM x 4 warps per SMSP.
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <cstdint>
 #include <cstdio>
 
 constexpr int kIters = 4096;
@@ -55,6 +57,34 @@ __global__ void k_mix(float* out, float seed) {  // 2 ex2 + 1 ffma2 per pair: MU
   out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
+// packed half-precision exponentials: 2 results per instruction
+__global__ void k_ex2_h2(float* out, float seed) {
+  uint32_t a[8];
+  for (int i = 0; i < 8; ++i) {
+    __half2 h = __floats2half2_rn(-(seed + i * 0.1f), -(seed + threadIdx.x * 1e-3f));
+    a[i] = *reinterpret_cast<uint32_t*>(&h);
+  }
+  for (int it = 0; it < kIters; ++it)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) asm volatile("ex2.approx.f16x2 %0, %0;" : "+r"(a[i]));
+  float s = 0;
+  for (int i = 0; i < 8; ++i) s += __low2float(*reinterpret_cast<__half2*>(&a[i]));
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+__global__ void k_ex2_bf2(float* out, float seed) {
+  uint32_t a[8];
+  for (int i = 0; i < 8; ++i) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(-(seed + i * 0.1f), -(seed + threadIdx.x * 1e-3f));
+    a[i] = *reinterpret_cast<uint32_t*>(&h);
+  }
+  for (int it = 0; it < kIters; ++it)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) asm volatile("ex2.approx.ftz.bf16x2 %0, %0;" : "+r"(a[i]));
+  float s = 0;
+  for (int i = 0; i < 8; ++i) s += __low2float(*reinterpret_cast<__nv_bfloat162*>(&a[i]));
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
 template <typename K>
 void run(const char* name, K kern, int ops_per_iter_per_thread, int threads, int sms, float* d) {
   cudaEvent_t a, b;
@@ -85,6 +115,8 @@ int main() {
     run("ffma", k_ffma, 8, th, sms, d);
     run("ffma2", k_ffma2, 16, th, sms, d);   // 2 FMA per lane per instruction
     run("mix", k_mix, 16, th, sms, d);       // ex2 count (2 per pair)
+    run("ex2_h2", k_ex2_h2, 16, th, sms, d);   // results (2 per instruction)
+    run("ex2_bf2", k_ex2_bf2, 16, th, sms, d);
   }
   return 0;
 }
