@@ -34,6 +34,7 @@ def main():
     ap.add_argument("--config", default="c4")
     ap.add_argument("--rows", type=int, default=4, help="random rows per rank (plus boundary rows)")
     ap.add_argument("--mode", default="nccl", choices=["nccl", "peer"])
+    ap.add_argument("--det", type=int, default=0, help="deterministic backward (query-stationary dQ kernel)")
     a = ap.parse_args()
     cfg = synth.CONFIGS[a.config]
     B, N, H, D = cfg["B"], cfg["N"], cfg["H"], cfg["D"]
@@ -50,6 +51,7 @@ def main():
     ctx = ua.Context(P=P, rank=rank, device=local)
     if P > 1:
         ctx.set_a2a_mode(a.mode)
+    ctx.set_deterministic(bool(a.det))
     c0, _ = ctx.comm_stats()
     r = ua.ulysses_attn_fwd(ctx, qs, ks, vs)
     dq, dk, dv = ua.ulysses_attn_bwd(ctx, qs, ks, vs, r.out, r.lse, ds)
@@ -102,7 +104,7 @@ def main():
         assert (s[0].abs() <= 1e-2 * mags[0] + 1e-3).all(), "sum_j dK_j != 0"
         assert (s[1].abs() <= 1e-2 * mags[1] + 1e-3).all(), "sum_j dV_j != sum_i dO_i"
         assert ((inner[0] - inner[1]).abs() <= 1e-2 * (imag[0] + imag[1]) + 1e-3).all(), "<Q,dQ> != <K,dK>"
-        print("BIG_OK", a.config, "P", P, flush=True)
+        print("BIG_OK", a.config, "P", P, "det" if a.det else "", flush=True)
     ctx.close()
     dist.barrier()
     dist.destroy_process_group()

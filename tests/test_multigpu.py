@@ -115,6 +115,18 @@ def test_bigconfig_p_way(config, P, mode):
     assert r.returncode == 0 and "BIG_OK" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
 
 
+@pytest.mark.gpu
+@pytest.mark.slow
+@pytest.mark.parametrize("config,P", [("c4", 1), ("c3", 2), ("c4", 4), ("c5", 4)])
+def test_bigconfig_deterministic(config, P):
+    """Full-size configs with the deterministic backward: sampled-row oracle parity + invariants."""
+    if torch.cuda.device_count() < P:
+        pytest.skip(f"needs {P} GPUs")
+    r = torchrun(P, os.path.join(ROOT, "tests", "mp_bigconfig_check.py"), f"--config={config}", "--det=1",
+                 timeout=1500)
+    assert r.returncode == 0 and "BIG_OK" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
+
+
 # ----------------------------------------------------------------- CPU, gloo
 GLOO_SCRIPT = r'''
 import os, sys, numpy as np, torch, torch.distributed as dist
