@@ -51,7 +51,7 @@ typedef enum {
   UA_ERR_INVALID_ARG = 1,       /* null / misaligned pointer, non-positive size, P != ctx P, workspace too small */
   UA_ERR_HEAD_DIVISIBILITY = 2, /* P > H or H % P != 0 (P:317 head limit) */
   UA_ERR_SEQ_DIVISIBILITY = 3,  /* N % P != 0; no padding */
-  UA_ERR_UNSUPPORTED = 4,       /* D not in {32, 64, 72, 128}; N >= 2^31; no sm_100 device; D = 72 with the peer transport */
+  UA_ERR_UNSUPPORTED = 4,       /* D not in {32, 64, 72, 128}; N >= 2^31; no sm_100 device */
   UA_ERR_CUDA = 5,
   UA_ERR_NCCL = 6
 } ua_status;

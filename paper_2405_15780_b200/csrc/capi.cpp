@@ -539,8 +539,6 @@ ua_status ua_ulysses_attn_fwd(ua_ctx* ctx, const void* q, const void* k, const v
                                 stream);
   }
 
-  if (ctx->a2a_mode == UA_A2A_PEER && D == 72)
-    return fail(UA_ERR_UNSUPPORTED, "peer all-to-all supports D in {32, 64, 128}; use the NCCL transport for D=72");
   if (ctx->a2a_mode == UA_A2A_PEER) {
     // Fused all-to-alls over NVLink peer stores (no NCCL on the data path).
     const size_t S = size_t(s.shard()) * 2;
@@ -666,8 +664,6 @@ ua_status ua_ulysses_attn_bwd(ua_ctx* ctx, const void* q, const void* k, const v
     return UA_OK;
   }
 
-  if (ctx->a2a_mode == UA_A2A_PEER && D == 72)
-    return fail(UA_ERR_UNSUPPORTED, "peer all-to-all supports D in {32, 64, 128}; use the NCCL transport for D=72");
   if (ctx->a2a_mode == UA_A2A_PEER) {
     // Fused all-to-alls over NVLink peer stores (no NCCL on the data path).
     const size_t S = size_t(s.shard()) * 2;

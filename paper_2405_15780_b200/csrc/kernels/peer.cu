@@ -122,6 +122,37 @@ __global__ void __launch_bounds__(256) finalize_push_kernel(const float4* __rest
   }
 }
 
+// Delta = rowsum(dO * O) in fp32, one (b, t, h) row per thread, into the head
+// owner's Delta block, for head dims whose rows are not a power-of-two number
+// of 16-B vectors (D = 72).  Same arithmetic (sequential fmaf over the row) as
+// layout.cu's delta_kernel, so the Delta bits do not depend on the transport.
+__global__ void __launch_bounds__(256) delta_push_kernel(PeerPack pk, int64_t B, int64_t Nl, int H, int Hl, int rank,
+                                                         int vpr, int64_t tensor_vecs) {
+  const int64_t rows = B * Nl * H;
+  const uint4* dout = static_cast<const uint4*>(pk.dout);
+  const uint4* out = static_cast<const uint4*>(pk.out);
+  for (int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < rows; r += int64_t(gridDim.x) * blockDim.x) {
+    const int h = int(r % H);
+    const int64_t t = (r / H) % Nl;
+    const int64_t b = r / (int64_t(H) * Nl);
+    const int j = h / Hl, hp = h % Hl;
+    float acc = 0.f;
+    for (int i = 0; i < vpr; ++i) {
+      uint4 a = dout[r * vpr + i], o = out[r * vpr + i];
+      const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&a);
+      const __nv_bfloat162* o2 = reinterpret_cast<const __nv_bfloat162*>(&o);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        float2 fa = __bfloat1622float2(a2[k]), fo = __bfloat1622float2(o2[k]);
+        acc = fmaf(fa.x, fo.x, acc);
+        acc = fmaf(fa.y, fo.y, acc);
+      }
+    }
+    float* dd = reinterpret_cast<float*>(static_cast<uint4*>(pk.dst[j]) + int64_t(pk.ntensors) * tensor_vecs);
+    dd[((int64_t(rank) * Nl + t) * B + b) * Hl + hp] = acc;
+  }
+}
+
 int grid_for(int64_t work, int threads) {
   int64_t g = (work + threads - 1) / threads;
   const int64_t cap = 148 * 16;
@@ -140,6 +171,14 @@ cudaError_t launch_pack_push(const PeerPack& pk, int64_t B, int64_t Nl, int H, i
     case 4: pack_push_kernel<4><<<grid, 256, 0, stream>>>(pk, B, Nl, H, Hl, rank, tensor_vecs); break;
     case 8: pack_push_kernel<8><<<grid, 256, 0, stream>>>(pk, B, Nl, H, Hl, rank, tensor_vecs); break;
     case 16: pack_push_kernel<16><<<grid, 256, 0, stream>>>(pk, B, Nl, H, Hl, rank, tensor_vecs); break;
+    case 9: {  // D = 72: rows of 9 vectors straddle warps; Delta in its own pass
+      PeerPack data = pk;
+      data.dout = nullptr;
+      pack_push_kernel<9><<<grid, 256, 0, stream>>>(data, B, Nl, H, Hl, rank, tensor_vecs);
+      if (pk.dout != nullptr)
+        delta_push_kernel<<<grid_for(B * Nl * H, 256), 256, 0, stream>>>(pk, B, Nl, H, Hl, rank, 9, tensor_vecs);
+      break;
+    }
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();

@@ -29,13 +29,11 @@ def torchrun(nproc, script, *args, timeout=900, env=None):
     (4, 4096, 8, 64, 1.0),
     (8, 8192, 16, 64, 1.0),
     (8, 2048, 8, 32, 2.0),
-    (2, 2048, 4, 72, 1.0),      # D=72 (NCCL transport; peer mode reports UNSUPPORTED)
+    (2, 2048, 4, 72, 1.0),      # D=72 (peer transport: Delta in its own push pass)
 ])
 def test_ulysses_p_way(P, N, H, D, sigma, mode):
     if torch.cuda.device_count() < P:
         pytest.skip(f"needs {P} GPUs")
-    if D == 72 and mode == "peer":
-        pytest.skip("peer transport: D in {32, 64, 128}")
     r = torchrun(P, os.path.join(ROOT, "tests", "mp_ulysses_check.py"), f"--N={N}", f"--H={H}", f"--D={D}",
                  f"--sigma={sigma}", f"--mode={mode}")
     assert r.returncode == 0 and "MP_OK" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
