@@ -134,18 +134,18 @@ from oracle import ulysses
 dist.init_process_group("gloo")
 rank, P = dist.get_rank(), dist.get_world_size()
 # 1) validation is host-only and identical on every rank (S:248 head limit)
-codes = [ua.lib().ua_validate(1, 16, 1, 64, P), ua.lib().ua_validate(1, 15, 4, 64, P),
-         ua.lib().ua_validate(1, 16, 4, 64, P)]
+codes = [ua.lib().ua_validate(1, 16, 1, 64, P), ua.lib().ua_validate(1, 15, P, 64, P),
+         ua.lib().ua_validate(1, 16, P, 64, P)]
 allc = [None] * P
 dist.all_gather_object(allc, codes)
 assert all(c == [2, 3, 0] for c in allc), allc
 # 1b) LSS validation: no head limit (P:317), same codes on every rank
-lcodes = [ua.lib().ua_lss_validate(1, 16, 1, 64, P), ua.lib().ua_lss_validate(1, 15, 4, 64, P)]
+lcodes = [ua.lib().ua_lss_validate(1, 16, 1, 64, P), ua.lib().ua_lss_validate(1, 15, P, 64, P)]
 allc = [None] * P
 dist.all_gather_object(allc, lcodes)
 assert all(c == [0, 3] for c in allc), allc
 # 2) the oracle's all-to-all (S:122) equals torch.distributed.all_to_all (library routine)
-B, N, H, D = 1, 8, 4, 2
+B, N, H, D = 1, 8, P, 2
 x = np.arange(B * N * H * D, dtype=np.float64).reshape(B, N, H, D)
 shards = ulysses.shard_seq(x, P)
 mine = torch.from_numpy(shards[rank].copy())
@@ -177,12 +177,14 @@ dist.destroy_process_group()
 '''
 
 
-def test_gloo_two_ranks(tmp_path):
+@pytest.mark.parametrize("P", [2, 8])
+def test_gloo_ranks(tmp_path, P):
+    """Host logic at world size 2 and 8 (the largest SP group of one box)."""
     from paper_2405_15780_b200 import build
     build.build()
     script = tmp_path / "gloo_check.py"
     script.write_text(GLOO_SCRIPT)
-    r = torchrun(2, str(script), timeout=300, env={"UA_ROOT": ROOT})
+    r = torchrun(P, str(script), timeout=600, env={"UA_ROOT": ROOT})
     assert r.returncode == 0 and "GLOO_OK" in r.stdout, r.stdout[-2000:] + r.stderr[-3000:]
 
 
