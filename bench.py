@@ -304,7 +304,10 @@ def main():
                 "flops_per_launch": bwd_f / P, "flops_formula": "10*B*N^2*(H/P)*D per launch (5 GEMMs incl. recompute)"}
     fwd_roof = {"kernel": "attn_fwd_kernel", "achieved": kf["tflops"], "frac": kf["tflops"] / peaks["bf16_sustained"],
                 "avg_ms": kf["avg_ms"]}
-    launches = sum(n for name, (ms, n) in phases.items() if not name.startswith("a2a"))
+    # our kernels per phase call: attn_bwd = bwd_prep + the backward kernel (+ the dQ kernel in
+    # deterministic mode); the other non-a2a phases launch one kernel each (a2a phases: NCCL)
+    per_call = {"attn_bwd": 3 if args.deterministic else 2}
+    launches = sum(n * per_call.get(name, 1) for name, (ms, n) in phases.items() if not name.startswith("a2a"))
     phase_ms = {name: ms / args.steps for name, (ms, n) in phases.items() if n}
     a2a_ms = sum(ms for name, (ms, n) in phases.items() if name.startswith("a2a"))
     a2a_bytes = bytes1 - bytes0
