@@ -11,15 +11,16 @@
 // all matrices are the same") — the price is recomputing S and dP (3 GEMMs per
 // tile pair instead of the fused kernel's one dQ GEMM).
 //
-// Design: one CTA = one 128-row query tile of one (b, h), 12 warps:
+// Design: one CTA = one 128-row query tile of one (b, h), 4 + 4 kGroups warps:
 //   warp 0      TMA producer (Q, dO once; K/V ring of kStages tiles)
 //   warp 1      tcgen05.mma issuer + TMEM owner
-//   warps 4-7   elementwise for key columns [0, 64) of each tile (thread = query row)
-//   warps 8-11  elementwise for key columns [64, 128)
+//   warps 4..   kGroups elementwise warpgroups, group g owns key columns
+//               [kCols g, kCols (g+1)) of each tile (thread = query row);
+//               kGroups = 4 (32 columns each, 4 warps per SM sub-partition) by default
 // TMEM: S[0] [0,128)  S[1] [128,256)  dP [256,384)  dQ [384, 384+D).
 //   S[j&1] = Q K_j^T and dP = dO V_j^T are SS MMAs; the elementwise warpgroups
 //   load both, release dP (the next dP GEMM may start), and write bf16 dS into
-//   their own half of S[j&1] (columns [64g, 64g+32)); dQ += dS K_j is a TS MMA
+//   the first kCols/2 of their own S[j&1] columns; dQ += dS K_j is a TS MMA
 //   (A = dS from TMEM, B = K_j MN-major, the same smem tile the S GEMM read
 //   K-major).  S is double-buffered, so S_{j+1} and dP_{j+1} run under the
 //   elementwise work of tile j.
@@ -29,6 +30,9 @@
 #include "attn_common.cuh"
 #include "attn_kernels.h"
 
+#ifndef UA_BWD_DQ_GROUPS
+#define UA_BWD_DQ_GROUPS 4     // elementwise warpgroups per query tile (2: 64 key columns each, 4: 32 each)
+#endif
 #ifndef UA_BWD_DQ_POLY_MOD
 #define UA_BWD_DQ_POLY_MOD 4   // every UA_BWD_DQ_POLY_MOD-th exp2 pair on the FMA pipe (D <= 64; 0: none)
 #endif
@@ -41,18 +45,24 @@ template <int D>
 struct BwdDqCfg {
   using G = TileGeom<D>;
   static constexpr int kStages = D == 128 ? 2 : 3;
-  static constexpr int kThreads = 384;
+  static constexpr int kGroups = UA_BWD_DQ_GROUPS;             // elementwise warpgroups
+  static constexpr int kCols = 128 / kGroups;                    // key columns per thread and tile
+  static constexpr int kThreads = 128 * (1 + kGroups);
   static constexpr int kSmemBytes = 1024 + (2 + 2 * kStages) * G::kTileBytes + 256;
   static constexpr uint32_t kColS = 0, kColDP = 256, kColDQ = 384;
   static constexpr bool kPolyExp = UA_BWD_DQ_POLY_MOD > 0 && D <= 64;
-  static constexpr int kRegsHigh = 224;
-  static constexpr int kRegsLow = ((65536 / 384 / 8 * 8) * 384 - 256 * kRegsHigh) / 128 / 8 * 8;
+  // setmaxnreg.inc can only take what the CTA's own warps released: the launch
+  // gives every thread kRegsLaunch, the producer / MMA warpgroup drops to kRegsLow.
+  static constexpr int kRegsLaunch = (65536 / kThreads) / 8 * 8 > 255 ? 248 : (65536 / kThreads) / 8 * 8;
+  static constexpr int kRegsLow = 56;
+  static constexpr int kRegsHigh = ((1 + kGroups) * kRegsLaunch - kRegsLow) / kGroups / 8 * 8 > 232
+                                       ? 232 : ((1 + kGroups) * kRegsLaunch - kRegsLow) / kGroups / 8 * 8;
   static_assert(kColDQ + D <= 512, "TMEM budget");
   static_assert(kSmemBytes <= 232448, "smem budget");
 };
 
 template <int D>
-__global__ void __launch_bounds__(384, 1) attn_bwd_dq_kernel(const __grid_constant__ BwdParams p) {
+__global__ void __launch_bounds__(BwdDqCfg<D>::kThreads, 1) attn_bwd_dq_kernel(const __grid_constant__ BwdParams p) {
   using C = BwdDqCfg<D>;
   using G = TileGeom<D>;
   constexpr int kStages = C::kStages;
@@ -85,9 +95,9 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dq_kernel(const __grid_consta
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&sdp_full[i], 1);
-      mbar_init(&ds_ready[i], 256);
+      mbar_init(&ds_ready[i], 128 * C::kGroups);
     }
-    mbar_init(dp_free, 256);
+    mbar_init(dp_free, 128 * C::kGroups);
     mbar_init(dq_done, 1);
     fence_mbar_init();
   }
@@ -136,8 +146,8 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dq_kernel(const __grid_consta
         tc_fence_after();
         const uint32_t kt = sKa + (j % kStages) * G::kTileBytes;
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk)  // dS keys [16kk, 16kk+16): warpgroup kk/4 stored them at 64*(kk/4)
-          mma_ts(tbase + C::kColDQ, tbase + C::kColS + jb * 128 + kk * 8 + (kk >= 4 ? 32 : 0),
+        for (int kk = 0; kk < 8; ++kk)  // dS keys [16kk, 16kk+16): packed by their warpgroup at the start of its columns
+          mma_ts(tbase + C::kColDQ, tbase + C::kColS + jb * 128 + (16 * kk / C::kCols) * C::kCols + (kk * 8) % (C::kCols / 2),
                  mnmajor_desc<D>(kt, kk), idesc_q, (j > 0 || kk > 0) ? 1u : 0u);
         mma_commit(&kv_empty[j % kStages]);
       };
@@ -171,7 +181,7 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dq_kernel(const __grid_consta
   } else if (warp >= 4) {
     // ------------------------------------------------------------ elementwise
     setmaxnreg_inc<C::kRegsHigh>();
-    const int g = (warp - 4) / 4;              // key-column half of every tile
+    const int g = (warp - 4) / 4;              // key columns [kCols g, kCols (g+1)) of every tile
     const int quad = warp % 4;
     const int r = quad * 32 + lane;            // query row within the tile
     const uint32_t t_lane = tbase + (uint32_t(quad * 32) << 16);
@@ -182,20 +192,21 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dq_kernel(const __grid_consta
     const float2 c2 = make_float2(p.scale_log2, p.scale_log2), nl2 = make_float2(nl, nl), nd2 = make_float2(nd, nd);
     for (int j = 0; j < n_kt; ++j) {
       const int jb = j & 1;
-      const uint32_t colS = C::kColS + jb * 128 + 64 * g;
+      const uint32_t colS = C::kColS + jb * 128 + C::kCols * g;
       mbar_wait(&sdp_full[jb], (j >> 1) & 1);
       tc_fence_after();
-      uint32_t rs[64], rd[64];
-      tmem_ld32(t_lane + colS, rs);
-      tmem_ld32(t_lane + colS + 32, rs + 32);
-      tmem_ld32(t_lane + C::kColDP + 64 * g, rd);
-      tmem_ld32(t_lane + C::kColDP + 64 * g + 32, rd + 32);
+      uint32_t rs[C::kCols], rd[C::kCols];
+#pragma unroll
+      for (int cc = 0; cc < C::kCols; cc += 32) {
+        tmem_ld32(t_lane + colS + cc, rs + cc);
+        tmem_ld32(t_lane + C::kColDP + C::kCols * g + cc, rd + cc);
+      }
       tmem_ld_wait();
       tc_fence_before();
       mbar_arrive(dp_free);
-      uint32_t pk[32];
+      uint32_t pk[C::kCols / 2];
 #pragma unroll
-      for (int i = 0; i < 32; ++i) {
+      for (int i = 0; i < C::kCols / 2; ++i) {
         const float2 arg = __ffma2_rn(make_float2(__uint_as_float(rs[2 * i]), __uint_as_float(rs[2 * i + 1])), c2, nl2);
         const bool poly = C::kPolyExp && (i % (UA_BWD_DQ_POLY_MOD > 0 ? UA_BWD_DQ_POLY_MOD : 1)) == 1;
         const float2 pp = poly ? exp2_poly2(arg) : make_float2(ex2(arg.x), ex2(arg.y));
@@ -203,7 +214,8 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dq_kernel(const __grid_consta
         const float2 ds = __fmul2_rn(pp, dd);
         pk[i] = pack_bf16x2(ds.x, ds.y);
       }
-      tmem_st32(t_lane + colS, pk);      // own columns only (already loaded)
+      if constexpr (C::kCols == 64) tmem_st32(t_lane + colS, pk);   // own columns only (already loaded)
+      else tmem_st16(t_lane + colS, pk);
       tmem_st_wait();
       tc_fence_before();
       mbar_arrive(&ds_ready[jb]);
@@ -216,7 +228,7 @@ __global__ void __launch_bounds__(384, 1) attn_bwd_dq_kernel(const __grid_consta
     float* dst = p.dq_acc + (bh * n_pad + q_row) * d_io;
 #pragma unroll
     for (int cc = 0; cc < D; cc += 16) {
-      if (((cc / 16) & 1) != g) continue;
+      if ((cc / 16) % C::kGroups != g) continue;
       uint32_t x[16];
       tmem_ld16(t_lane + C::kColDQ + cc, x);
       tmem_ld_wait();
