@@ -39,6 +39,9 @@
 #ifndef UA_BWD_SEP_P
 #define UA_BWD_SEP_P 1      // dQ-less variant: separate TMEM P^T, next S^T under the exponentials
 #endif
+#ifndef UA_BWD_EW_SPLIT
+#define UA_BWD_EW_SPLIT 0   // D <= 64 with dQ: two elementwise warpgroups of 32 query columns per half (24 warps); A/B: 853 vs 874 TFLOP/s at c4
+#endif
 #ifndef UA_BWD_SEP_POLY_MOD
 #define UA_BWD_SEP_POLY_MOD 0   // same as UA_BWD_POLY_MOD for the separate-P^T variant (A/B: none is best)
 #endif
@@ -84,9 +87,14 @@ struct BwdWsCfg {
 // Separate-P^T pipeline of the dQ-less variant (needs 64 spare TMEM columns).
 template <int D, bool kDq>
 __host__ __device__ constexpr bool ws_sep_p() { return !kDq && BwdWsCfg<D>::kSepPFits && UA_BWD_SEP_P; }
-// kSepP: 20 warps -- each 64-query half has two elementwise warpgroups of 32 query columns.
+// Column split of the elementwise work: each 64-query half has two warpgroups of
+// 32 query columns (kSepP: 20 warps; with the dQ drain warpgroup: 24 warps).
 template <int D, bool kDq>
-__host__ __device__ constexpr int ws_threads() { return ws_sep_p<D, kDq>() ? 640 : 512; }
+__host__ __device__ constexpr bool ws_ew_split() { return kDq && UA_BWD_EW_SPLIT && D <= 64; }
+template <int D, bool kDq>
+__host__ __device__ constexpr int ws_threads() {
+  return ws_sep_p<D, kDq>() ? 640 : (ws_ew_split<D, kDq>() ? 768 : 512);
+}
 
 // kDq = false (deterministic mode): dK, dV only; dQ comes from the query-stationary
 // attn_bwd_dq_kernel (attn_bwd_dq.cu), so no dS^T staging, dQ GEMM or reduction here.
@@ -95,7 +103,10 @@ __global__ void __launch_bounds__(ws_threads<D, kDq>(), 1) attn_bwd_ws_kernel(co
   using C = BwdWsCfg<D>;
   constexpr bool kAlias = C::kAliasDq && kDq;   // dQ shares TMEM with dP^T (D = 128)
   constexpr bool kSepP = ws_sep_p<D, kDq>();
-  constexpr int kEwArrive = kSepP ? 256 : 128;   // arrivals per half on s_loaded / p_ready / ds_ready
+  constexpr bool kSplit = kSepP || ws_ew_split<D, kDq>();   // two elementwise warpgroups per half
+  constexpr int kEwArrive = kSplit ? 256 : 128;   // arrivals per half on s_loaded / p_ready / ds_ready
+  constexpr int kEwCols = kSplit ? 32 : 64;       // query columns per elementwise thread and half tile
+  constexpr int kEwEnd = kSplit ? 20 : 12;        // first warp after the elementwise warpgroups
   using G = TileGeom<D>;
   constexpr int kSl = C::kSlots;
   extern __shared__ uint8_t smem_raw[];
@@ -170,8 +181,11 @@ __global__ void __launch_bounds__(ws_threads<D, kDq>(), 1) attn_bwd_ws_kernel(co
   // warpgroup gives 40 of them to the four elementwise warpgroups (56 + 4 x 104
   // <= 5 x 96: setmaxnreg.inc can only take what the CTA's own warps released).
   // Each role branch re-balances first thing so ptxas sees which limit applies.
-#define UA_BWD_REGS_LOW() do { if constexpr (kSepP) setmaxnreg_dec<56>(); } while (0)
+// 24-warp split with dQ: 768 threads launch with 80 registers; 56 (producer / MMA)
+// + 4 x 80 (elementwise) + 104 (dQ drain) = 6 x 80.
+#define UA_BWD_REGS_LOW() do { if constexpr (kSplit) setmaxnreg_dec<56>(); } while (0)
 #define UA_BWD_REGS_HIGH() do { if constexpr (kSepP) setmaxnreg_inc<104>(); } while (0)
+#define UA_BWD_REGS_DRAIN() do { if constexpr (kSplit) setmaxnreg_inc<104>(); } while (0)
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer
@@ -350,11 +364,12 @@ __global__ void __launch_bounds__(ws_threads<D, kDq>(), 1) attn_bwd_ws_kernel(co
             const uint32_t acc = (t > 0 || hh > 0) ? 1u : 0u;
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk)
-              mma_ts(tbase + C::kColDV, tbase + C::kColS + 64 * hh + kk * 8, mnmajor_desc_r<D, 64>(do_at(U), kk),
-                     idesc_g, (acc || kk > 0) ? 1u : 0u);
+              mma_ts(tbase + C::kColDV, tbase + C::kColS + 64 * hh + kk * 8 + (kSplit && kk >= 2 ? 16 : 0),
+                     mnmajor_desc_r<D, 64>(do_at(U), kk), idesc_g, (acc || kk > 0) ? 1u : 0u);
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk)
-              mma_ts(tbase + C::kColDK, tbase + C::kColDP + 64 * hh + kk * 8, mnmajor_desc_r<D, 64>(q_at(U), kk),
+              mma_ts(tbase + C::kColDK, tbase + C::kColDP + 64 * hh + kk * 8 + (kSplit && kk >= 2 ? 16 : 0),
+                     mnmajor_desc_r<D, 64>(q_at(U), kk),
                      idesc_g, (acc || kk > 0) ? 1u : 0u);
             mma_commit(&slot_empty[U % kSl]);
             UA_TEV(1, T, 3 + 4 * hh);
@@ -394,11 +409,11 @@ __global__ void __launch_bounds__(ws_threads<D, kDq>(), 1) attn_bwd_ws_kernel(co
       }  // !kSepP
     }
     __syncwarp();
-  } else if (warp >= 4 && warp < (kSepP ? 20 : 12)) {
+  } else if (warp >= 4 && warp < kEwEnd) {
     // ------------------------------------------------------------ elementwise (half hh)
     UA_BWD_REGS_HIGH();
-    const int hh = kSepP ? (warp - 4) / 8 : (warp - 4) / 4;
-    const int g = kSepP ? ((warp - 4) / 4) % 2 : 0;   // kSepP: query columns [32g, 32g+32) of the half
+    const int hh = kSplit ? (warp - 4) / 8 : (warp - 4) / 4;
+    const int g = kSplit ? ((warp - 4) / 4) % 2 : 0;   // kSplit: query columns [32g, 32g+32) of the half
     const int quad = warp % 4;
     const int j = quad * 32 + lane;  // key row within the tile
     const uint32_t t_lane = tbase + (uint32_t(quad * 32) << 16);
@@ -505,7 +520,7 @@ __global__ void __launch_bounds__(ws_threads<D, kDq>(), 1) attn_bwd_ws_kernel(co
         if (j == 0) UA_TEV(2 + hh, T, 2);
         tc_fence_after();
         const uint32_t atom = smem_u32(sdS + (T % C::kNumDs) * C::kDsBytes + hh * (128 * 128) + j * 128);
-        const uint32_t nl_s = smem_u32(sLsed + s * 128);
+        const uint32_t nl_s = smem_u32(sLsed + s * 128 + 32 * g);
         const uint32_t nd_s = nl_s + 64 * 4;
 #pragma unroll
         // TMEM loads software-pipelined: chunk k+1's S^T / dP^T columns are in
@@ -516,10 +531,10 @@ __global__ void __launch_bounds__(ws_threads<D, kDq>(), 1) attn_bwd_ws_kernel(co
         tmem_ld16(t_lane + colDP, rdA);
         tmem_ld_wait();
 #pragma unroll
-        for (int cc = 0; cc < 64; cc += 16) {
+        for (int cc = 0; cc < kEwCols; cc += 16) {
           uint32_t* rs = ((cc / 16) & 1) ? rsB : rsA;
           uint32_t* rd = ((cc / 16) & 1) ? rdB : rdA;
-          if (cc + 16 < 64) {
+          if (cc + 16 < kEwCols) {
             tmem_ld16(t_lane + colS + cc + 16, ((cc / 16) & 1) ? rsA : rsB);
             tmem_ld16(t_lane + colDP + cc + 16, ((cc / 16) & 1) ? rdA : rdB);
           }
@@ -545,10 +560,10 @@ __global__ void __launch_bounds__(ws_threads<D, kDq>(), 1) attn_bwd_ws_kernel(co
           tmem_st8(t_lane + colDP + cc / 2, pk_ds);
 #pragma unroll
           for (int qd = 0; qd < 2 * int(kDq); ++qd) {
-            const int chunk = ((cc / 8) + qd) ^ (j & 7);
+            const int chunk = (4 * g + (cc / 8) + qd) ^ (j & 7);
             sts128(atom + chunk * 16, pk_ds[4 * qd], pk_ds[4 * qd + 1], pk_ds[4 * qd + 2], pk_ds[4 * qd + 3]);
           }
-          if (cc + 16 < 64) tmem_ld_wait();
+          if (cc + 16 < kEwCols) tmem_ld_wait();
         }
         fence_proxy_async_smem();
         tmem_st_wait();
@@ -606,11 +621,12 @@ __global__ void __launch_bounds__(ws_threads<D, kDq>(), 1) attn_bwd_ws_kernel(co
       tc_fence_before();
       mbar_arrive(acc_free);
     }
-  } else if (kDq && warp >= 12) {
+  } else if (kDq && warp >= kEwEnd) {
     // ------------------------------------------------------------ dQ drain
     const int quad = warp % 4;
     const int r = quad * 32 + lane;  // query row within the tile
-    const bool leader = threadIdx.x == 384;
+    UA_BWD_REGS_DRAIN();
+    const bool leader = threadIdx.x == kEwEnd * 32;
     const uint32_t t_lane = tbase + (uint32_t(quad * 32) << 16);
     // columns held in registers per round; D = 80 drains 96 columns (3 boxes of 32: the
     // TMA reduce drops columns >= 72 as out of bounds, TMEM columns 496..511 are spare)
@@ -674,6 +690,7 @@ __global__ void __launch_bounds__(ws_threads<D, kDq>(), 1) attn_bwd_ws_kernel(co
   }
 #undef UA_BWD_REGS_LOW
 #undef UA_BWD_REGS_HIGH
+#undef UA_BWD_REGS_DRAIN
 
   tc_fence_before();
   __syncthreads();
