@@ -1,5 +1,5 @@
 // attn_bwd_ws.cu — persistent, warp-specialised attention backward (sm_100a),
-// D in {32, 64, 128}.
+// D in {32, 64, 80 (= head dim 72 padded), 128}.
 //
 // Mathematics as attn_bwd.cu:
 //   P = exp(S - lse), dV += P^T dO, dS = P (dP - Delta), dK += scale dS^T Q,
@@ -26,6 +26,15 @@
 //   dK [256+D, +D)  dQ [256+2D, +D) for D <= 64.  D = 128 has no room for dQ:
 //   it aliases dP^T [128, 256) and the next tile's dP^T GEMMs wait for the dQ
 //   drain (the S^T GEMMs of the next tile run meanwhile).
+// Variants (template kDq, macros):
+//  * kDq = false (deterministic mode, ua_ctx_set_deterministic): no dQ GEMM /
+//    staging / drain -- attn_bwd_dq.cu computes dQ query-stationary.  Every
+//    item sweeps from query tile 0 (grid-independent dK / dV order).  For
+//    D <= 80 the freed dQ columns hold a separate bf16 P^T per half (kSepP), the
+//    next S^T GEMM is issued once S^T is in registers, and each half has two
+//    elementwise warpgroups of 32 query columns (20 warps).
+//  * UA_BWD_EW_SPLIT (off): the same 32-column split with the dQ path (24 warps).
+//  * UA_BWD_KV_TMEM, UA_BWD_POLY_MOD, UA_BWD_STAGGER: see below.
 #include "attn_common.cuh"
 #include "attn_kernels.h"
 #include "trace.cuh"
