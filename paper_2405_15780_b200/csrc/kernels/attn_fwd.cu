@@ -54,6 +54,9 @@
 #ifndef UA_FWD_MAXNREG
 #define UA_FWD_MAXNREG 224  // >0: setmaxnreg the softmax warpgroups up to this many registers (0: off)
 #endif
+#ifndef UA_FWD_POLY_MAXD
+#define UA_FWD_POLY_MAXD 128  // largest head dim whose softmax offloads exp2 pairs to the FMA pipe (A/B at D = 128: +0.4-1.4 %)
+#endif
 #ifndef UA_FWD_RELOAD
 #define UA_FWD_RELOAD 0     // two TMEM passes over S (max, then exp); A/B: slower, kept as an option
 #endif
@@ -88,7 +91,7 @@ struct FwdCfg {
   static constexpr uint32_t kPStride = kSeparateP ? 64 : 128;
   static constexpr uint32_t kColO = kSeparateP ? 384 : 256;     // + t*D
   static constexpr float kRescaleThreshold = 8.0f;  // log2 units
-  static constexpr bool kPolyExp = D <= 64;          // exp unit co-binds only at small D
+  static constexpr bool kPolyExp = D <= UA_FWD_POLY_MAXD;  // FMA-pipe exp2 share for head dims up to this
 };
 
 template <int D>
