@@ -160,6 +160,10 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        # torchrun sets OMP_NUM_THREADS=1 per rank; rank 0 runs the oracle alone, on all host cores
+        import oracle
+        oracle.set_num_threads(len(os.sched_getaffinity(0)))
     n_sample = 8192
     W, K = args.warmup, args.steps
     base = cpu_baseline(steps=1, n_sample=n_sample)  # warm-up compile / first touch

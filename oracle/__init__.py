@@ -62,6 +62,7 @@ def _load():
             lib.oracle_attn_bwd.argtypes = [d, d, d, d, i64, i64, i64, i64, d, d, d, d, d, d]
             lib.oracle_attn_bwd_dq_rows.argtypes = [d, d, ctypes.POINTER(i64), i64, d, d, i64, i64, i64, i64, d]
             lib.oracle_num_threads.restype = ctypes.c_int
+            lib.oracle_set_num_threads.argtypes = [ctypes.c_int]
             _lib = lib
     return _lib
 
@@ -76,6 +77,11 @@ def _ptr(a: np.ndarray):
 
 def num_threads() -> int:
     return int(_load().oracle_num_threads())
+
+
+def set_num_threads(n: int) -> None:
+    """OpenMP thread count of the oracle's loops (no effect on its arithmetic)."""
+    _load().oracle_set_num_threads(int(n))
 
 
 def attn_fwd(q, k, v, with_abs: bool = False):

@@ -58,6 +58,16 @@ static double dot(const double* a, const double* b, int64_t D) {
   return acc;
 }
 
+/* Thread count of the OpenMP loops (harness plumbing, no arithmetic): the bench's
+ * reference arm runs alone on rank 0 under torchrun, which sets OMP_NUM_THREADS=1. */
+void oracle_set_num_threads(int n) {
+#ifdef _OPENMP
+  if (n > 0) omp_set_num_threads(n);
+#else
+  (void)n;
+#endif
+}
+
 int oracle_num_threads(void) {
 #ifdef _OPENMP
   return omp_get_max_threads();
