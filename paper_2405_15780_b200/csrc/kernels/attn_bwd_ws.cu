@@ -51,6 +51,9 @@
 #ifndef UA_BWD_EW_SPLIT
 #define UA_BWD_EW_SPLIT 0   // D <= 64 with dQ: two elementwise warpgroups of 32 query columns per half (24 warps); A/B: 853 vs 874 TFLOP/s at c4
 #endif
+#ifndef UA_BWD_LDBATCH
+#define UA_BWD_LDBATCH 0    // with dQ, no column split: all 64 S^T / dP^T columns of a half loaded with one wait (A/B: 838 vs 869 TFLOP/s at c4, spills)
+#endif
 #ifndef UA_BWD_SEP_POLY_MOD
 #define UA_BWD_SEP_POLY_MOD 0   // same as UA_BWD_POLY_MOD for the separate-P^T variant (A/B: none is best)
 #endif
@@ -116,6 +119,7 @@ __global__ void __launch_bounds__(ws_threads<D, kDq>(), 1) attn_bwd_ws_kernel(co
   constexpr int kEwArrive = kSplit ? 256 : 128;   // arrivals per half on s_loaded / p_ready / ds_ready
   constexpr int kEwCols = kSplit ? 32 : 64;       // query columns per elementwise thread and half tile
   constexpr int kEwEnd = kSplit ? 20 : 12;        // first warp after the elementwise warpgroups
+  constexpr bool kBatch = kDq && !kSplit && UA_BWD_LDBATCH;   // 128 data registers per elementwise thread
   using G = TileGeom<D>;
   constexpr int kSl = C::kSlots;
   extern __shared__ uint8_t smem_raw[];
@@ -192,9 +196,10 @@ __global__ void __launch_bounds__(ws_threads<D, kDq>(), 1) attn_bwd_ws_kernel(co
   // Each role branch re-balances first thing so ptxas sees which limit applies.
 // 24-warp split with dQ: 768 threads launch with 80 registers; 56 (producer / MMA)
 // + 4 x 80 (elementwise) + 104 (dQ drain) = 6 x 80.
-#define UA_BWD_REGS_LOW() do { if constexpr (kSplit) setmaxnreg_dec<56>(); } while (0)
-#define UA_BWD_REGS_HIGH() do { if constexpr (kSepP) setmaxnreg_inc<104>(); } while (0)
-#define UA_BWD_REGS_DRAIN() do { if constexpr (kSplit) setmaxnreg_inc<104>(); } while (0)
+// kBatch (512 threads at 128): 56 + 2 x 168 (elementwise) + 112 (dQ drain) <= 4 x 128.
+#define UA_BWD_REGS_LOW() do { if constexpr (kSplit || kBatch) setmaxnreg_dec<56>(); } while (0)
+#define UA_BWD_REGS_HIGH() do { if constexpr (kSepP) setmaxnreg_inc<104>(); else if constexpr (kBatch) setmaxnreg_inc<168>(); } while (0)
+#define UA_BWD_REGS_DRAIN() do { if constexpr (kSplit) setmaxnreg_inc<104>(); else if constexpr (kBatch) setmaxnreg_dec<112>(); } while (0)
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer
@@ -535,17 +540,27 @@ __global__ void __launch_bounds__(ws_threads<D, kDq>(), 1) attn_bwd_ws_kernel(co
         // TMEM loads software-pipelined: chunk k+1's S^T / dP^T columns are in
         // flight while chunk k is computed (P^T / dS^T stores only ever touch
         // columns already read).
-        uint32_t rsA[16], rdA[16], rsB[16], rdB[16];
-        tmem_ld16(t_lane + colS, rsA);
-        tmem_ld16(t_lane + colDP, rdA);
+        // kBatch: the half's 64 S^T and 64 dP^T columns in four loads and one
+        // wait (all exponentials of the half independent); else two 16-column
+        // buffers, chunk k+1 in flight while chunk k is computed.
+        uint32_t rsv[kBatch ? 64 : 32], rdv[kBatch ? 64 : 32];
+        if constexpr (kBatch) {
+          tmem_ld32(t_lane + colS, rsv);
+          tmem_ld32(t_lane + colS + 32, rsv + 32);
+          tmem_ld32(t_lane + colDP, rdv);
+          tmem_ld32(t_lane + colDP + 32, rdv + 32);
+        } else {
+          tmem_ld16(t_lane + colS, *reinterpret_cast<uint32_t(*)[16]>(rsv));
+          tmem_ld16(t_lane + colDP, *reinterpret_cast<uint32_t(*)[16]>(rdv));
+        }
         tmem_ld_wait();
 #pragma unroll
         for (int cc = 0; cc < kEwCols; cc += 16) {
-          uint32_t* rs = ((cc / 16) & 1) ? rsB : rsA;
-          uint32_t* rd = ((cc / 16) & 1) ? rdB : rdA;
-          if (cc + 16 < kEwCols) {
-            tmem_ld16(t_lane + colS + cc + 16, ((cc / 16) & 1) ? rsA : rsB);
-            tmem_ld16(t_lane + colDP + cc + 16, ((cc / 16) & 1) ? rdA : rdB);
+          uint32_t* rs = kBatch ? rsv + cc : rsv + 16 * ((cc / 16) & 1);
+          uint32_t* rd = kBatch ? rdv + cc : rdv + 16 * ((cc / 16) & 1);
+          if (!kBatch && cc + 16 < kEwCols) {
+            tmem_ld16(t_lane + colS + cc + 16, *reinterpret_cast<uint32_t(*)[16]>(rsv + 16 * (((cc / 16) & 1) ^ 1)));
+            tmem_ld16(t_lane + colDP + cc + 16, *reinterpret_cast<uint32_t(*)[16]>(rdv + 16 * (((cc / 16) & 1) ^ 1)));
           }
           uint32_t pk_p[8], pk_ds[8];
 #pragma unroll
@@ -572,7 +587,7 @@ __global__ void __launch_bounds__(ws_threads<D, kDq>(), 1) attn_bwd_ws_kernel(co
             const int chunk = (4 * g + (cc / 8) + qd) ^ (j & 7);
             sts128(atom + chunk * 16, pk_ds[4 * qd], pk_ds[4 * qd + 1], pk_ds[4 * qd + 2], pk_ds[4 * qd + 3]);
           }
-          if (cc + 16 < kEwCols) tmem_ld_wait();
+          if (!kBatch && cc + 16 < kEwCols) tmem_ld_wait();
         }
         fence_proxy_async_smem();
         tmem_st_wait();
