@@ -51,6 +51,9 @@
 #ifndef UA_BWD_EW_SPLIT
 #define UA_BWD_EW_SPLIT 0   // D <= 64 with dQ: two elementwise warpgroups of 32 query columns per half (24 warps); A/B: 853 vs 874 TFLOP/s at c4
 #endif
+#ifndef UA_BWD_DQ_LATE
+#define UA_BWD_DQ_LATE 1    // issue the dQ GEMM after the next tile's S^T / dP^T GEMMs of the second half
+#endif
 #ifndef UA_BWD_LDBATCH
 #define UA_BWD_LDBATCH 0    // with dQ, no column split: all 64 S^T / dP^T columns of a half loaded with one wait (A/B: 838 vs 869 TFLOP/s at c4, spills)
 #endif
@@ -387,7 +390,7 @@ __global__ void __launch_bounds__(ws_threads<D, kDq>(), 1) attn_bwd_ws_kernel(co
                      idesc_g, (acc || kk > 0) ? 1u : 0u);
             mma_commit(&slot_empty[U % kSl]);
             UA_TEV(1, T, 3 + 4 * hh);
-            if (kDq && hh == 1) {  // dQ(T) = dS K
+            auto issue_dq = [&]() {  // dQ(T) = dS K
               if (!C::kAliasDq && T > 0) {
                 UA_TEV(1, T, 9);
                 mbar_wait(dq_empty, (T - 1) & 1);
@@ -402,7 +405,12 @@ __global__ void __launch_bounds__(ws_threads<D, kDq>(), 1) attn_bwd_ws_kernel(co
               mma_commit(dq_full);
               UA_TEV(1, T, 11);
               mma_commit(&ds_free[T % C::kNumDs]);
-            }
+            };
+            // Without the dQ / dP^T aliasing, the next tile's S^T / dP^T GEMMs of this
+            // half go first (their sdp_full commit then does not wait for the dQ GEMM,
+            // which reads only smem and its own TMEM columns): UA_BWD_DQ_LATE.
+            constexpr bool kDqLate = UA_BWD_DQ_LATE && !kAlias;
+            if (kDq && hh == 1 && !kDqLate) issue_dq();
             if (t + 1 < n_q) {  // next tile, this half
               wait_slot(2 * (T + 1) + hh);
               issue_s(T + 1, hh);
@@ -415,6 +423,7 @@ __global__ void __launch_bounds__(ws_threads<D, kDq>(), 1) attn_bwd_ws_kernel(co
                 issue_dp(T + 1, 1);
               }
             }
+            if (kDq && hh == 1 && kDqLate) issue_dq();
           }
         }
         mma_commit(acc_full);
