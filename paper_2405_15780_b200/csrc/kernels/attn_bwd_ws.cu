@@ -54,6 +54,9 @@
 #ifndef UA_BWD_DQ_LATE
 #define UA_BWD_DQ_LATE 1    // issue the dQ GEMM after the next tile's S^T / dP^T GEMMs of the second half
 #endif
+#ifndef UA_BWD_BOX2
+#define UA_BWD_BOX2 0       // D <= 64: two dQ staging boxes (both halves of a tile's dQ reduced concurrently)
+#endif
 #ifndef UA_BWD_LDBATCH
 #define UA_BWD_LDBATCH 0    // with dQ, no column split: all 64 S^T / dP^T columns of a half loaded with one wait (A/B: 838 vs 869 TFLOP/s at c4, spills)
 #endif
@@ -81,11 +84,12 @@ struct BwdWsCfg {
   static constexpr bool kKvTmem = UA_BWD_KV_TMEM && D <= 64;
   static constexpr uint32_t kColK = 256 + 3 * D, kColV = 256 + 3 * D + D / 2;
   static constexpr int kHalfBytes = 64 * D * 2;               // one [64][D] bf16 half tile
-  static constexpr int kSlots = D == 128 ? 3 : (D == 80 ? 4 : 6);  // half-tile ring depth
+  // half-tile ring depth; UA_BWD_BOX2 trades one D <= 64 slot for a second dQ staging box
+  static constexpr int kSlots = D == 128 ? 3 : (D == 80 ? 4 : (UA_BWD_BOX2 && D == 64 ? 5 : 6));
   static constexpr int kSlotBytes = 2 * kHalfBytes;            // Q_h + dO_h
   static constexpr int kNumDs = kAliasDq ? 1 : 2;              // dS^T smem buffers
   static constexpr int kDsBytes = 128 * 128 * 2;
-  static constexpr int kStageBoxes = D == 128 ? 2 : 1;         // 16 KB fp32 staging boxes for dQ
+  static constexpr int kStageBoxes = (D == 128 || (UA_BWD_BOX2 && D <= 64)) ? 2 : 1;  // 16 KB fp32 staging boxes for dQ
   static constexpr int kBoxBytes = 128 * 32 * 4;
   static constexpr int kLsedBytes = 128 * 4;                   // per slot: 64 x -lse*log2e, 64 x -Delta
   static constexpr bool kPolyExp = UA_BWD_POLY_MOD > 0;
