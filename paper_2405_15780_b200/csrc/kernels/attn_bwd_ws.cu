@@ -55,7 +55,7 @@
 #define UA_BWD_DQ_LATE 1    // issue the dQ GEMM after the next tile's S^T / dP^T GEMMs of the second half
 #endif
 #ifndef UA_BWD_BOX2
-#define UA_BWD_BOX2 0       // D <= 64: two dQ staging boxes (both halves of a tile's dQ reduced concurrently)
+#define UA_BWD_BOX2 0       // D = 64: two dQ staging boxes (both halves of a tile's dQ reduced concurrently)
 #endif
 #ifndef UA_BWD_LDBATCH
 #define UA_BWD_LDBATCH 0    // with dQ, no column split: all 64 S^T / dP^T columns of a half loaded with one wait (A/B: 838 vs 869 TFLOP/s at c4, spills)
@@ -89,7 +89,7 @@ struct BwdWsCfg {
   static constexpr int kSlotBytes = 2 * kHalfBytes;            // Q_h + dO_h
   static constexpr int kNumDs = kAliasDq ? 1 : 2;              // dS^T smem buffers
   static constexpr int kDsBytes = 128 * 128 * 2;
-  static constexpr int kStageBoxes = (D == 128 || (UA_BWD_BOX2 && D <= 64)) ? 2 : 1;  // 16 KB fp32 staging boxes for dQ
+  static constexpr int kStageBoxes = (D == 128 || (UA_BWD_BOX2 && D == 64)) ? 2 : 1;  // 16 KB fp32 staging boxes for dQ
   static constexpr int kBoxBytes = 128 * 32 * 4;
   static constexpr int kLsedBytes = 128 * 4;                   // per slot: 64 x -lse*log2e, 64 x -Delta
   static constexpr bool kPolyExp = UA_BWD_POLY_MOD > 0;
