@@ -128,3 +128,13 @@ def test_lss_workspace_plan():
     assert ua.lss_workspace_size(1, 4096, 2, 64, 4)[0] > 0
     with pytest.raises(ua.HeadDivisibilityError):
         ua.workspace_size(1, 4096, 2, 64, 4)
+
+
+def test_ctx_mode_setters_validate_arguments():
+    """Host-side argument checks of the ctx mode entry points (no device needed)."""
+    import ctypes
+    L = ua.lib()
+    assert L.ua_ctx_set_deterministic(None, 1) == 1          # UA_ERR_INVALID_ARG
+    assert L.ua_ctx_get_deterministic(None, ctypes.byref(ctypes.c_int(0))) == 1
+    assert L.ua_ctx_set_a2a_mode(None, 0) == 1
+    assert "ctx" in L.ua_last_error().decode()
