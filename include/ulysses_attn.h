@@ -66,7 +66,7 @@ const char* ua_last_error(void);
  * Pure host check of a problem shape, no device access (S:238, S:244, S:248,
  * S:276).  Checked in this order: B, N, H, D, P >= 1 else
  * INVALID_ARG; P > H or H % P else HEAD_DIVISIBILITY; N % P else
- * SEQ_DIVISIBILITY; D not in {32,64,128} or N >= 2^31 else UNSUPPORTED. */
+ * SEQ_DIVISIBILITY; D not in {32,64,72,128} or N >= 2^31 else UNSUPPORTED. */
 ua_status ua_validate(int64_t B, int64_t N, int H, int D, int P);
 
 /* Workspace bytes the fwd / bwd calls need for this shape (0 for the forward
