@@ -6,8 +6,9 @@ package.  It shares no code with the CUDA path (``paper_2405_15780_b200``) and
 never imports it; the product never imports this package.
 
 Contents
-  * ``attn_fwd``, ``attn_fwd_rows``, ``attn_bwd`` — ctypes wrappers over
-    ``oracle.c`` (plain fp64 loops + OpenMP; definitions and citations there).
+  * ``attn_fwd``, ``attn_fwd_rows``, ``attn_bwd``, ``attn_bwd_dq_rows``,
+    ``attn_bwd_kv_rows`` — ctypes wrappers over ``oracle.c`` (plain fp64 loops +
+    OpenMP; definitions and citations there).  ``delta`` — Delta = rowsum(dO*O).
   * ``ulysses`` — the paper's sequence-parallel data movement (§2.5):
     sequence shards, the all-to-all, head shards, and the
     composition seq-shard -> a2a -> per-head attention -> a2a back.
@@ -61,6 +62,7 @@ def _load():
                                                  i64, i64, i64, i64, d, d]
             lib.oracle_attn_bwd.argtypes = [d, d, d, d, i64, i64, i64, i64, d, d, d, d, d, d]
             lib.oracle_attn_bwd_dq_rows.argtypes = [d, d, ctypes.POINTER(i64), i64, d, d, i64, i64, i64, i64, d]
+            lib.oracle_attn_bwd_kv_rows.argtypes = [d, d, d, d, i64, i64, ctypes.POINTER(i64), i64, d, d]
             lib.oracle_num_threads.restype = ctypes.c_int
             lib.oracle_set_num_threads.argtypes = [ctypes.c_int]
             _lib = lib
@@ -128,6 +130,32 @@ def attn_bwd_dq_rows(qrows, dorows, bh, k, v):
     _load().oracle_attn_bwd_dq_rows(_ptr(qrows), _ptr(dorows), bh.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), R,
                                     _ptr(k), _ptr(v), B, Nk, H, D, _ptr(out))
     return out
+
+
+def attn_bwd_kv_rows(qh, kh, vh, doh, keys):
+    """Exact (dK_j, dV_j) for the listed key rows of ONE head of self-attention:
+    qh, kh, vh, doh [N][D] (that head's rows).  Recomputes lse_i and Delta_i for
+    every query with the oracle's own fp64 forward.  Returns (dk_rows, dv_rows)
+    [R][D].  Cost O(N^2 D) per call (the forward pass over the head)."""
+    qh, kh, vh, doh = _f64(qh), _f64(kh), _f64(vh), _f64(doh)
+    keys = np.ascontiguousarray(np.asarray(keys, dtype=np.int64))
+    N, D = qh.shape
+    assert kh.shape == (N, D) and vh.shape == (N, D) and doh.shape == (N, D)
+    assert keys.ndim == 1 and (keys >= 0).all() and (keys < N).all()
+    R = keys.shape[0]
+    dk = np.empty((R, D), dtype=np.float64)
+    dv = np.empty((R, D), dtype=np.float64)
+    _load().oracle_attn_bwd_kv_rows(_ptr(qh), _ptr(kh), _ptr(vh), _ptr(doh), N, D,
+                                    keys.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), R, _ptr(dk), _ptr(dv))
+    return dk, dv
+
+
+def delta(dout, out):
+    """Delta_i = dO_i . O_i per (b, token, head) (the row term of
+    dS = P (dP - Delta)), fp64, [B][N][H][D] -> [B][N][H]."""
+    dout, out = _f64(dout), _f64(out)
+    assert dout.shape == out.shape
+    return (dout * out).sum(axis=-1)
 
 
 def attn_bwd(q, k, v, dout, with_abs: bool = False):

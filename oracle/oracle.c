@@ -294,3 +294,52 @@ void oracle_attn_bwd_dq_rows(const double* qrows, const double* dorows, const in
     free(o);
   }
 }
+
+/* Exact dK_j, dV_j for R explicit key rows of ONE head (full-size parity of the
+ * backward at sizes where the dense backward is out of reach).  qh, kh, vh, doh
+ * are that head's [N][D] rows (self-attention, N queries = N keys).  Follows the
+ * definitions above in order: pass 1 recomputes, for every query i, lse_i and
+ * o_i (attend_row, the oracle's own fp64 forward) and Delta_i = dO_i . o_i;
+ * then for each requested key j:
+ *   dV_j = sum_i P_ij dO_i,  dK_j = scale sum_i P_ij (dO_i . v_j - Delta_i) q_i,
+ * with P_ij = exp(s_ij - lse_i), s_ij = scale q_i . k_j. */
+void oracle_attn_bwd_kv_rows(const double* qh, const double* kh, const double* vh, const double* doh, int64_t N,
+                             int64_t D, const int64_t* keys, int64_t R, double* dk_rows, double* dv_rows) {
+  const double scale = 1.0 / sqrt((double)D);
+  double* lse = (double*)malloc(sizeof(double) * (size_t)(N > 0 ? N : 1));
+  double* delta = (double*)malloc(sizeof(double) * (size_t)(N > 0 ? N : 1));
+#pragma omp parallel
+  {
+    double* s = (double*)malloc(sizeof(double) * (size_t)(N > 0 ? N : 1));
+    double* o = (double*)malloc(sizeof(double) * (size_t)D);
+#pragma omp for schedule(dynamic, 16)
+    for (int64_t i = 0; i < N; ++i) {
+      lse[i] = attend_row(qh + i * D, kh, vh, N, D, D, scale, s, o, NULL);
+      delta[i] = dot(doh + i * D, o, D);
+    }
+    free(s);
+    free(o);
+  }
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t r = 0; r < R; ++r) {
+    const int64_t j = keys[r];
+    const double* kj = kh + j * D;
+    const double* vj = vh + j * D;
+    double* dk = dk_rows + r * D;
+    double* dv = dv_rows + r * D;
+    for (int64_t d = 0; d < D; ++d) dk[d] = dv[d] = 0.0;
+    for (int64_t i = 0; i < N; ++i) {
+      const double* qi = qh + i * D;
+      const double* doi = doh + i * D;
+      const double p = exp(scale * dot(qi, kj, D) - lse[i]);
+      const double ds = p * (dot(doi, vj, D) - delta[i]);
+      for (int64_t d = 0; d < D; ++d) {
+        dv[d] += p * doi[d];
+        dk[d] += ds * qi[d];
+      }
+    }
+    for (int64_t d = 0; d < D; ++d) dk[d] *= scale;
+  }
+  free(lse);
+  free(delta);
+}

@@ -362,6 +362,49 @@ def test_bwd_dq_rows_matches_dense():
     assert np.abs(got - dq[bh[:, 0], idx, bh[:, 1]]).max() < 1e-13
 
 
+def test_bwd_kv_rows_matches_dense():
+    """Sampled key rows (first, last, interior) of two heads against the dense
+    backward, which torch autograd and finite differences pin above."""
+    B, N, H, D = 1, 75, 3, 16
+    q, k, v, do = (rnd((B, N, H, D), s, 1.5) for s in (120, 121, 122, 123))
+    _, dk, dv, _, _ = oracle.attn_bwd(q, k, v, do)
+    keys = np.array([0, 74, 37, 8, 8])
+    for h in (0, 2):
+        gk, gv = oracle.attn_bwd_kv_rows(q[0, :, h], k[0, :, h], v[0, :, h], do[0, :, h], keys)
+        assert np.abs(gk - dk[0, keys, h]).max() < 1e-13
+        assert np.abs(gv - dv[0, keys, h]).max() < 1e-13
+
+
+def test_bwd_kv_rows_against_torch_autograd():
+    """Independent of oracle.c's dense backward: torch fp64 autograd of
+    <softmax(QK^T/sqrt(D)) V, dO> for one head."""
+    N, D = 40, 8
+    q, k, v, do = (rnd((N, D), s) for s in (130, 131, 132, 133))
+    tq, tk, tv = (torch.tensor(x, requires_grad=True) for x in (q, k, v))
+    p = torch.softmax(tq @ tk.T / math.sqrt(D), dim=-1)
+    ((p @ tv) * torch.from_numpy(do)).sum().backward()
+    keys = np.arange(N)
+    gk, gv = oracle.attn_bwd_kv_rows(q, k, v, do, keys)
+    assert np.abs(gk - tk.grad.numpy()).max() < 1e-12
+    assert np.abs(gv - tv.grad.numpy()).max() < 1e-12
+
+
+def test_delta_is_probability_weighted_dp():
+    """Delta_i = dO_i . o_i = sum_j P_ij (dO_i . v_j) (rows of P sum to 1), with
+    o from torch SDPA and P from a materialised torch softmax; dO = 0 -> 0."""
+    B, N, H, D = 1, 30, 2, 8
+    q, k, v, do = (rnd((B, N, H, D), s) for s in (140, 141, 142, 143))
+    o = torch_sdpa(q, k, v)
+    got = oracle.delta(do, o)
+    s = torch.einsum("bihd,bjhd->bhij", torch.from_numpy(q), torch.from_numpy(k)) / math.sqrt(D)
+    p = torch.softmax(s, dim=-1).numpy()
+    dp = np.einsum("bihd,bjhd->bhij", do, v)
+    ref = np.einsum("bhij,bhij->bih", p, dp)
+    assert got.shape == (B, N, H)
+    assert np.abs(got - ref).max() < 1e-12
+    assert np.array_equal(oracle.delta(np.zeros_like(do), o), np.zeros((B, N, H)))
+
+
 # ------------------------------------------------------------------ layer pins
 @pytest.mark.parametrize("B,N,H,D", [(1, 12, 2, 4), (2, 7, 3, 2)])
 def test_layer_matches_torch_autograd(B, N, H, D):
