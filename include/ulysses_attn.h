@@ -171,6 +171,68 @@ ua_status ua_ulysses_attn_bwd(ua_ctx* ctx, const void* q, const void* k, const v
                               const float* lse, const void* dout, void* dq, void* dk, void* dv, int64_t B, int64_t N,
                               int H, int D, int P, void* workspace, size_t workspace_bytes, ua_stream_t stream);
 
+/* ------------------------------------------------------------- rank-local steps
+ * The Ulysses path of ua_ulysses_attn_fwd / _bwd one step at a time, with no
+ * communication: what ONE rank r of P computes between the all-to-alls
+ * (§2.5; SURVEY §8(a) rows A1, A3, A6, B1, B3+B4, B6).  The fwd /
+ * bwd entry points run exactly these internals; the all-to-all between them is
+ * a byte-exact permutation (output[j] on rank i == input[i] on rank j),
+ * so a caller holding every rank's buffers (e.g. a single-GPU test simulating P
+ * ranks) can perform it with plain copies.  None of these calls needs a ctx;
+ * all are stream-ordered and asynchronous; shapes are checked with
+ * ua_validate(B, N, H, D, P) first, pointers must be non-NULL and 16-B aligned
+ * (else UA_ERR_INVALID_ARG).  Layouts (elements, row-major, Hl = H/P, Nl = N/P):
+ *
+ * ua_pack_seq_to_head (A1; B1 with Delta): for w < ntensors (0..4)
+ *   src[w] : bf16 [B][Nl][H][D]      this rank's sequence shard
+ *   dst[w] : bf16 [P][Nl][B][Hl][D]  send chunk j = heads [j Hl, (j+1) Hl) of every local token
+ *   dout, out, delta: all NULL, or all non-NULL: delta fp32 [P][Nl][B][Hl] =
+ *            sum_d dout*out in fp32 (Delta_i = dO_i . O_i), packed like the
+ *            tensors.  ntensors may be 0 when delta is requested.
+ *   After the all-to-all, rank j's receive buffer [P][Nl][B][Hl][D] (chunk i
+ *   from rank i) IS the head-shard tensor [N][B][Hl][D] the attention reads.
+ * ua_unpack_head_to_seq (A6, B6): for w < ntensors (1..4)
+ *   src[w] : bf16 [P][Nl][B][Hl][D]  chunk s = head block s, received from rank s
+ *   dst[w] : bf16 [B][Nl][H][D]
+ * ua_push_seq_to_head (A1+A2, B1+B3's input exchange fused; the UA_A2A_PEER
+ * transport's kernel): stores rank `rank`'s chunks straight into every
+ * destination's receive buffer: dst_rank[j] (j < P; device pointers this
+ * process can write: a peer mapping, or local memory) holds
+ * [ntensors][N][B][Hl][D] bf16 followed (if dout, out non-NULL) by Delta
+ * [N][B][Hl] fp32; rank `rank`'s tokens land at rows [rank Nl, (rank+1) Nl).
+ * No flag or fence is raised (the transport adds those).
+ *
+ * ua_head_attn_fwd (A3): exact attention of rank `rank`'s head shard
+ * (heads [rank Hl, (rank+1) Hl)) over all N tokens:
+ *   q, k, v : bf16 [N][B][Hl][D]     the all-to-all #1 receive buffers
+ *   o       : bf16 [N][B][Hl][D]     = the all-to-all #2 send buffer (token block i -> rank i)
+ *   lse     : fp32 [B][Hl][N]
+ *   o_owner : NULL, or P pointers: then o must be NULL and the epilogue stores
+ *             each output row straight into its token owner's [B][Nl][H][D]
+ *             tensor o_owner[n / Nl] (A3 + A5 fused, UA_A2A_PEER).
+ * ua_head_attn_bwd (B3 + B4): the backward of that head shard
+ *   q, k, v, dout : bf16 [N][B][Hl][D];  lse fp32 [B][Hl][N];  delta fp32 [N][B][Hl]
+ *   dq, dk, dv    : bf16 [N][B][Hl][D] (= the all-to-all #4 send buffers), or
+ *   owners        : NULL, or 3P pointers (dq owners, dk owners, dv owners; each
+ *                   [B][Nl][H][D]); then dq, dk, dv must be NULL and every row goes
+ *                   straight to its token owner (B3 + B5 fused, UA_A2A_PEER).
+ *   deterministic : as ua_ctx_set_deterministic.
+ *   workspace     : >= ua_head_attn_bwd_workspace_size bytes (fp32 dQ accumulator
+ *                   and the per-row (lse, Delta) table). */
+ua_status ua_pack_seq_to_head(const void* const* src, void* const* dst, int ntensors, int64_t B, int64_t N, int H,
+                              int D, int P, const void* dout, const void* out, float* delta, ua_stream_t stream);
+ua_status ua_unpack_head_to_seq(const void* const* src, void* const* dst, int ntensors, int64_t B, int64_t N, int H,
+                                int D, int P, ua_stream_t stream);
+ua_status ua_push_seq_to_head(const void* const* src, int ntensors, void* const* dst_rank, int64_t B, int64_t N, int H,
+                              int D, int P, int rank, const void* dout, const void* out, ua_stream_t stream);
+ua_status ua_head_attn_fwd(const void* q, const void* k, const void* v, void* o, float* lse, int64_t B, int64_t N,
+                           int H, int D, int P, int rank, void* const* o_owner, ua_stream_t stream);
+ua_status ua_head_attn_bwd_workspace_size(int64_t B, int64_t N, int H, int D, int P, size_t* bytes);
+ua_status ua_head_attn_bwd(const void* q, const void* k, const void* v, const void* dout, const float* lse,
+                           const float* delta, void* dq, void* dk, void* dv, int64_t B, int64_t N, int H, int D, int P,
+                           int rank, void* const* owners, int deterministic, void* workspace, size_t workspace_bytes,
+                           ua_stream_t stream);
+
 /* ------------------------------------------------------------- LSS chunking
  * One contiguous key segment ("Long Sequence Segmentation"):
  * exact attention of all N queries of a head-sharded problem over keys

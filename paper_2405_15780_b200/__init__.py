@@ -32,7 +32,9 @@ EXPORTS = ("ua_version", "ua_status_string", "ua_last_error", "ua_validate", "ua
            "ua_ctx_set_deterministic", "ua_ctx_get_deterministic",
            "ua_ulysses_attn_fwd", "ua_ulysses_attn_bwd", "ua_attn_fwd_segment", "ua_lse_merge",
            "ua_f32_to_bf16_bnhd", "ua_lss_validate", "ua_lss_workspace_size", "ua_lss_attn_fwd", "ua_lss_attn_bwd",
-           "ua_layer_sizes", "ua_layer_fwd", "ua_layer_bwd")
+           "ua_layer_sizes", "ua_layer_fwd", "ua_layer_bwd",
+           "ua_pack_seq_to_head", "ua_unpack_head_to_seq", "ua_push_seq_to_head", "ua_head_attn_fwd",
+           "ua_head_attn_bwd_workspace_size", "ua_head_attn_bwd")
 
 PHASES = ("pack_fwd", "a2a_fwd_in", "attn_fwd", "a2a_fwd_out", "unpack_fwd", "pack_bwd", "a2a_bwd_in",
           "attn_bwd", "dq_finalize", "a2a_bwd_out", "unpack_bwd")
@@ -92,6 +94,14 @@ def lib():
         L.ua_attn_fwd_segment.argtypes = [vp, vp, vp, vp, vp, i64, i64, i32, i32, i64, i64, vp]
         L.ua_lse_merge.argtypes = [vp, vp, vp, vp, i64, i32, vp]
         L.ua_f32_to_bf16_bnhd.argtypes = [vp, vp, i64, i64, i32, i32, vp]
+        pp = ctypes.POINTER(vp)
+        L.ua_pack_seq_to_head.argtypes = [pp, pp, i32, i64, i64, i32, i32, i32, vp, vp, vp, vp]
+        L.ua_unpack_head_to_seq.argtypes = [pp, pp, i32, i64, i64, i32, i32, i32, vp]
+        L.ua_push_seq_to_head.argtypes = [pp, i32, pp, i64, i64, i32, i32, i32, i32, vp, vp, vp]
+        L.ua_head_attn_fwd.argtypes = [vp, vp, vp, vp, vp, i64, i64, i32, i32, i32, i32, pp, vp]
+        L.ua_head_attn_bwd_workspace_size.argtypes = [i64, i64, i32, i32, i32, ctypes.POINTER(sz)]
+        L.ua_head_attn_bwd.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp, i64, i64, i32, i32, i32, i32, pp, i32, vp,
+                                       sz, vp]
         for name in EXPORTS:
             getattr(L, name).restype = getattr(L, name).restype if name in (
                 "ua_version", "ua_status_string", "ua_last_error") else i32
@@ -398,6 +408,78 @@ def lss_chunked_fwd(q, k, v, seg_len: int, stream=None):
         attn_fwd_segment(q, k, v, j0, min(j0 + seg_len, N), o_tmp, l_tmp, stream=stream)
         lse_merge(o_acc, l_acc, o_tmp, l_tmp, stream=stream)
     return f32_to_bf16_bnhd(o_acc, stream=stream), l_acc
+
+
+# ---------------------------------------------------------------- rank-local steps
+# (include/ulysses_attn.h "rank-local steps": what one rank computes between the
+# all-to-alls; no communication, no ctx.)
+def _ptr_array(ts):
+    return (ctypes.c_void_p * max(1, len(ts)))(*[t.data_ptr() if t is not None else 0 for t in ts])
+
+
+def pack_seq_to_head(srcs, P: int, dout=None, out=None, stream=None):
+    """A1 / B1: srcs = list of bf16 [B][N/P][H][D] shards of one rank.  Returns
+    (send list of bf16 [P][N/P][B][H/P][D], delta fp32 [P][N/P][B][H/P] or None)."""
+    ref = srcs[0] if srcs else dout
+    B, Nl, H, D = ref.shape
+    dsts = [torch.empty((P, Nl, B, H // P, D), dtype=torch.bfloat16, device=ref.device) for _ in srcs]
+    delta = None
+    if dout is not None:
+        delta = torch.empty((P, Nl, B, H // P), dtype=torch.float32, device=ref.device)
+    _check(lib().ua_pack_seq_to_head(_ptr_array(srcs), _ptr_array(dsts), len(srcs), B, Nl * P, H, D, P, _ptr(dout),
+                                     _ptr(out), _ptr(delta), _stream(stream)))
+    return dsts, delta
+
+
+def unpack_head_to_seq(srcs, P: int, stream=None):
+    """A6 / B6: srcs = list of bf16 [P][N/P][B][H/P][D] (chunk s from rank s).
+    Returns list of bf16 [B][N/P][H][D]."""
+    _, Nl, B, Hl, D = srcs[0].shape
+    H = Hl * P
+    dsts = [torch.empty((B, Nl, H, D), dtype=torch.bfloat16, device=srcs[0].device) for _ in srcs]
+    _check(lib().ua_unpack_head_to_seq(_ptr_array(srcs), _ptr_array(dsts), len(srcs), B, Nl * P, H, D, P,
+                                       _stream(stream)))
+    return dsts
+
+
+def push_seq_to_head(srcs, dst_ranks, P: int, rank: int, dout=None, out=None, stream=None):
+    """A1 + A2 fused (the peer transport's kernel): store rank `rank`'s chunks into
+    every destination's receive buffer dst_ranks[j] (uint8 tensors of
+    ntensors*N*B*Hl*D*2 (+ N*B*Hl*4 with Delta) bytes)."""
+    B, Nl, H, D = srcs[0].shape
+    _check(lib().ua_push_seq_to_head(_ptr_array(srcs), len(srcs), _ptr_array(dst_ranks), B, Nl * P, H, D, P, rank,
+                                     _ptr(dout), _ptr(out), _stream(stream)))
+
+
+def head_attn_fwd(q, k, v, P: int, rank: int, o=None, lse=None, o_owner=None, stream=None):
+    """A3 on rank `rank`'s head shard: q, k, v bf16 [N][B][H/P][D].  Returns (o
+    [N][B][H/P][D], or None when o_owner (P token-owner tensors [B][N/P][H][D]) is
+    given; lse fp32 [B][H/P][N])."""
+    N, B, Hl, D = q.shape
+    if lse is None:
+        lse = torch.empty((B, Hl, N), dtype=torch.float32, device=q.device)
+    if o is None and o_owner is None:
+        o = torch.empty_like(q)
+    owners = _ptr_array(o_owner) if o_owner is not None else None
+    _check(lib().ua_head_attn_fwd(_ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse), B, N, Hl * P, D, P, rank, owners,
+                                  _stream(stream)))
+    return o, lse
+
+
+def head_attn_bwd(q, k, v, dout, lse, delta, P: int, rank: int, owners=None, deterministic=False, stream=None):
+    """B3 + B4 on rank `rank`'s head shard (layouts as head_attn_fwd; delta fp32
+    [N][B][H/P]).  Returns (dq, dk, dv) bf16 [N][B][H/P][D], or None when owners
+    (3P token-owner tensors: dq owners, dk owners, dv owners) is given."""
+    N, B, Hl, D = q.shape
+    n = ctypes.c_size_t(0)
+    _check(lib().ua_head_attn_bwd_workspace_size(B, N, Hl * P, D, P, ctypes.byref(n)))
+    ws = torch.empty(max(n.value, 256), dtype=torch.uint8, device=q.device)
+    grads = (None, None, None) if owners is not None else tuple(torch.empty_like(q) for _ in range(3))
+    _check(lib().ua_head_attn_bwd(_ptr(q), _ptr(k), _ptr(v), _ptr(dout), _ptr(lse), _ptr(delta), _ptr(grads[0]),
+                                  _ptr(grads[1]), _ptr(grads[2]), B, N, Hl * P, D, P, rank,
+                                  _ptr_array(owners) if owners is not None else None, 1 if deterministic else 0,
+                                  _ptr(ws), ws.numel(), _stream(stream)))
+    return None if owners is not None else grads
 
 
 class UlyssesAttention(torch.autograd.Function):

@@ -130,29 +130,26 @@ FwdPlan plan_fwd(const Shape& s) {
   return p;
 }
 struct BwdPlan {
-  size_t send = 0, send_delta = 0, recv = 0, recv_delta = 0, dq_acc = 0, grad = 0, delta = 0, lsed = 0, total = 0;
+  size_t send = 0, send_delta = 0, recv = 0, recv_delta = 0, grad = 0, delta = 0, head = 0, total = 0;
 };
+size_t head_bwd_bytes(const Shape& s);
 BwdPlan plan_bwd(const Shape& s) {
   BwdPlan p;
   const size_t S = size_t(s.shard()) * 2;
   const size_t DL = size_t(s.B * s.Nl * s.H) * 4;  // Delta of one shard
-  const int64_t n_pad = (s.N + 127) / 128 * 128;
-  const size_t DQ = size_t(s.B * s.Hl * n_pad * s.D) * 4;  // fp32 dQ accumulator, rows padded to 128
   if (s.P == 1) {
     p.delta = 0;                                  // [N][B][H] fp32
-    p.dq_acc = align_up(DL);                      // [B*H][N_pad][D] fp32
-    p.lsed = align_up(p.dq_acc + DQ);             // [B*H][N_pad] float2 (-lse*log2e, Delta)
-    p.total = align_up(p.lsed + size_t(s.B * s.Hl * n_pad) * 8);
+    p.head = align_up(DL);                        // head_bwd workspace: dq_acc, (lse, Delta) table
+    p.total = align_up(p.head + head_bwd_bytes(s));
     return p;
   }
   p.send = 0;                                     // [4][P][Nl][B][Hl][D]; reused as recv_grad [3][P]...
   p.send_delta = align_up(4 * S);                 // [P][Nl][B][Hl]
   p.recv = align_up(p.send_delta + DL);           // [4][N][B][Hl][D]
   p.recv_delta = align_up(p.recv + 4 * S);        // [N][B][Hl]
-  p.dq_acc = align_up(p.recv_delta + DL);         // [B*Hl][N_pad][D] fp32
-  p.grad = align_up(p.dq_acc + DQ);               // [3][N][B][Hl][D] bf16
-  p.lsed = align_up(p.grad + 3 * S);              // [B*Hl][N_pad] float2
-  p.total = align_up(p.lsed + size_t(s.B * s.Hl * n_pad) * 8);
+  p.grad = align_up(p.recv_delta + DL);           // [3][N][B][Hl][D] bf16
+  p.head = align_up(p.grad + 3 * S);
+  p.total = align_up(p.head + head_bwd_bytes(s));
   return p;
 }
 
@@ -202,6 +199,16 @@ ua_status a2a(ua_ctx* ctx, void* const* send, void* const* recv, int nt, size_t 
 }
 
 ua_status check_async(ua_ctx* ctx) {
+  if (ctx) {  // kernels launch on the current device; a ctx is bound to one
+    int dev = -1;
+    cudaGetDevice(&dev);
+    if (dev != ctx->device)
+      return fail(UA_ERR_INVALID_ARG, "current CUDA device %d is not the ctx's device %d (cudaSetDevice first)", dev,
+                  ctx->device);
+  }
+  if (ctx && ctx->peer_err_host && *static_cast<volatile int*>(ctx->peer_err_host) != 0)
+    return fail(UA_ERR_CUDA, "a peer all-to-all wait timed out (a peer rank failed, died or diverged); "
+                             "outputs of that call are undefined and this ctx must be destroyed");
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(UA_ERR_CUDA, "pending CUDA error: %s", cudaGetErrorString(e));
   if (ctx && ctx->comm) {
@@ -292,7 +299,7 @@ ua_status launch_attention_bwd(Rows q, const void* dout, const void* k, const vo
   p.scale_log2 = float(1.4426950408889634 / std::sqrt(double(D)));
   p.d_io = D;
   p.deterministic = deterministic;
-  UA_CUDA(ua::launch_attn_bwd(p, D, int(B), heads, stream));
+  UA_CUDA(ua::launch_attn_bwd_ws(p, D, stream));
   return UA_OK;
 }
 
@@ -376,6 +383,72 @@ ua::PeerOut peer_out(const ua_ctx::PeerBuf& pb, size_t offset, const Shape& s, i
 
 enum { kSlotFwdIn = 0, kSlotFwdOut = 1, kSlotBwdIn = 2, kSlotBwdOut = 3 };
 
+// ------------------------------------------------------------ rank-local steps
+// Strides (elements) of the bf16 tensors a head-shard step reads: the a2a receive
+// layout [N][B][Hl][D], or the user layout [B][N][H][D] at P = 1.
+struct Strides {
+  int64_t sn, sh, sb;
+};
+Strides head_layout(int64_t B, int Hl, int D) { return {B * int64_t(Hl) * D, D, int64_t(Hl) * D}; }
+
+// A3 on one rank's head shard: O into the view o (a2a #2 send layout) or, with
+// o_peer, straight into the token owners' tensors (A3 + A5 fused).
+ua_status head_fwd(ua_ctx* ctx, const void* q, const void* k, const void* v, Strides st, void* o,
+                   const ua::PeerOut* o_peer, float* lse, int64_t B, int64_t N, int Hl, int D, cudaStream_t stream) {
+  const ua::ViewArg ov{o_peer ? nullptr : o, st.sn, st.sh, st.sb};
+  Phase ph(ctx, UA_PHASE_ATTN_FWD, stream);
+  return launch_attention_fwd(q, k, v, st.sn, st.sh, st.sb, ov, nullptr, 0, 0, 0, lse, N, int64_t(Hl) * N, B, N, Hl,
+                              D, 0, N, stream, o_peer);
+}
+
+// Workspace of head_bwd: fp32 dQ accumulator [B*Hl][N_pad][D] + (lse, Delta) table [B*Hl][N_pad].
+struct HeadBwdPlan {
+  size_t dq_acc = 0, lsed = 0, total = 0;
+};
+HeadBwdPlan plan_head_bwd(int64_t B, int64_t N, int Hl, int D) {
+  HeadBwdPlan p;
+  const int64_t n_pad = (N + 127) / 128 * 128;
+  p.lsed = align_up(size_t(B * Hl * n_pad * D) * 4);
+  p.total = align_up(p.lsed + size_t(B * Hl * n_pad) * 8);
+  return p;
+}
+size_t head_bwd_bytes(const Shape& s) { return plan_head_bwd(s.B, s.N, s.Hl, s.D).total; }
+
+// B3 + B4 on one rank's head shard: delta [N][B][Hl] (strides B*Hl, 1, Hl);
+// dq, dk, dv into views with the inputs' strides, or (peers = {dq, dk, dv}
+// owner maps) straight into the token owners' tensors (B3 + B5 fused).
+ua_status head_bwd(ua_ctx* ctx, const void* q, const void* k, const void* v, const void* dout, Strides st,
+                   const float* lse, const float* delta, void* dq, void* dk, void* dv, const ua::PeerOut* peers,
+                   int64_t B, int64_t N, int Hl, int D, int deterministic, char* ws, cudaStream_t stream) {
+  const HeadBwdPlan plan = plan_head_bwd(B, N, Hl, D);
+  float* dq_acc = reinterpret_cast<float*>(ws + plan.dq_acc);
+  const int64_t n_pad = (N + 127) / 128 * 128;
+  const float scale = float(1.0 / std::sqrt(double(D)));
+  {
+    Phase ph(ctx, UA_PHASE_ATTN_BWD, stream);
+    UA_CUDA(cudaMemsetAsync(dq_acc, 0, size_t(B * Hl * n_pad * D) * 4, stream));
+    const ua::ViewArg vdk{peers ? nullptr : dk, st.sn, st.sh, st.sb}, vdv{peers ? nullptr : dv, st.sn, st.sh, st.sb};
+    UA_TRY(launch_attention_bwd(q, k, v, dout, st.sn, st.sh, st.sb, vdk, vdv, dq_acc, lse, N, int64_t(Hl) * N, delta,
+                                B * int64_t(Hl), 1, Hl, B, N, Hl, D, reinterpret_cast<float2*>(ws + plan.lsed),
+                                deterministic, stream, peers ? &peers[1] : nullptr, peers ? &peers[2] : nullptr));
+  }
+  Phase ph(ctx, UA_PHASE_DQ_FINALIZE, stream);
+  if (peers) {
+    UA_CUDA(ua::launch_finalize_push(dq_acc, peers[0], B, N, Hl, D, scale, stream));
+  } else {
+    UA_CUDA(ua::launch_dq_finalize(dq_acc, ua::ViewArg{dq, st.sn, st.sh, st.sb}, B, N, Hl, D, scale, stream));
+  }
+  return UA_OK;
+}
+
+ua_status check_ptrs(std::initializer_list<const void*> ptrs) {
+  for (const void* ptr : ptrs) {
+    if (!ptr) return fail(UA_ERR_INVALID_ARG, "null tensor pointer");
+    if (!aligned16(ptr)) return fail(UA_ERR_INVALID_ARG, "tensor pointers must be 16-byte aligned");
+  }
+  return UA_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -458,6 +531,11 @@ ua_status ua_ctx_set_a2a_mode(ua_ctx* ctx, int mode) {
   if (mode == UA_A2A_PEER) {
     if (ctx->P == 1) return fail(UA_ERR_UNSUPPORTED, "peer all-to-all needs P > 1");
     if (ctx->P > ua::kMaxPeers) return fail(UA_ERR_UNSUPPORTED, "peer all-to-all supports P <= %d", ua::kMaxPeers);
+    if (!ctx->peer_err_host) {
+      UA_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&ctx->peer_err_host), sizeof(int), cudaHostAllocMapped));
+      *ctx->peer_err_host = 0;
+      UA_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&ctx->peer_err), ctx->peer_err_host, 0));
+    }
     if (!ctx->flags.local) {
       cudaStream_t s;
       UA_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
@@ -490,11 +568,15 @@ ua_status ua_ctx_get_a2a_mode(const ua_ctx* ctx, int* mode) {
 
 ua_status ua_ctx_destroy(ua_ctx* ctx) {
   if (!ctx) return UA_OK;
+  int prev = -1;
+  cudaGetDevice(&prev);
+  if (prev != ctx->device) cudaSetDevice(ctx->device);  // release on the ctx's device, restore below
   if (ctx->flags.local) {
     cudaDeviceSynchronize();
     for (auto* pb : {&ctx->flags, &ctx->fwd_in, &ctx->fwd_out, &ctx->bwd_in, &ctx->bwd_out}) peer_release(ctx, *pb);
   }
   ua_internal::layer_release(ctx);
+  if (ctx->peer_err_host) cudaFreeHost(ctx->peer_err_host);
   ncclResult_t r = ncclSuccess;
   if (ctx->comm) r = ncclCommDestroy(ctx->comm);
   for (auto& rec : ctx->pending) {
@@ -502,7 +584,9 @@ ua_status ua_ctx_destroy(ua_ctx* ctx) {
     cudaEventDestroy(rec.b);
   }
   for (cudaEvent_t e : ctx->pool) cudaEventDestroy(e);
+  const int dev = ctx->device;
   delete ctx;
+  if (prev >= 0 && prev != dev) cudaSetDevice(prev);
   if (r != ncclSuccess) return fail(UA_ERR_NCCL, "ncclCommDestroy: %s", ncclGetErrorString(r));
   return UA_OK;
 }
@@ -531,13 +615,7 @@ ua_status ua_ulysses_attn_fwd(ua_ctx* ctx, const void* q, const void* k, const v
   UA_TRY(check_device());
   UA_TRY(check_async(ctx));
 
-  if (P == 1) {
-    const int64_t sn = int64_t(H) * D, sh = D, sb = N * H * D;
-    ua::ViewArg o{out, sn, sh, sb};
-    Phase ph(ctx, UA_PHASE_ATTN_FWD, stream);
-    return launch_attention_fwd(q, k, v, sn, sh, sb, o, nullptr, 0, 0, 0, lse, N, int64_t(H) * N, B, N, H, D, 0, N,
-                                stream);
-  }
+  if (P == 1) return head_fwd(ctx, q, k, v, Strides{int64_t(H) * D, D, N * H * D}, out, nullptr, lse, B, N, H, D, stream);
 
   if (ctx->a2a_mode == UA_A2A_PEER) {
     // Fused all-to-alls over NVLink peer stores (no NCCL on the data path).
@@ -558,23 +636,22 @@ ua_status ua_ulysses_attn_fwd(ua_ctx* ctx, const void* q, const void* k, const v
     {
       Phase ph(ctx, UA_PHASE_A2A_FWD_IN, stream);
       UA_CUDA(ua::launch_wait_copy(static_cast<const int64_t*>(ctx->flags.local), kSlotFwdIn, P, step, nullptr,
-                                   nullptr, 0, stream));
+                                   nullptr, 0, ctx->peer_err, stream));
       ctx->a2a_calls += 1;
       ctx->a2a_bytes += int64_t(P - 1) * int64_t(s.chunk()) * 2 * 3;
     }
-    const int64_t sn = B * int64_t(s.Hl) * D, sh = D, sb = int64_t(s.Hl) * D;
     char* rin = static_cast<char*>(ctx->fwd_in.local);
     const ua::PeerOut po = peer_out(ctx->fwd_out, 0, s, ctx->rank);
-    {  // 3+4. attention; the epilogue stores O rows into the token owners' buffers
-      Phase ph(ctx, UA_PHASE_ATTN_FWD, stream);
-      UA_TRY(launch_attention_fwd(rin, rin + S, rin + 2 * S, sn, sh, sb, ua::ViewArg{nullptr, 0, 0, 0}, nullptr, 0, 0,
-                                  0, lse, N, int64_t(s.Hl) * N, B, N, s.Hl, D, 0, N, stream, &po));
+    // 3+4. attention; the epilogue stores O rows into the token owners' buffers
+    UA_TRY(head_fwd(ctx, rin, rin + S, rin + 2 * S, head_layout(B, s.Hl, D), nullptr, &po, lse, B, N, s.Hl, D, stream));
+    {
+      Phase ph(ctx, UA_PHASE_A2A_FWD_OUT, stream);
       UA_CUDA(ua::launch_signal(fl, kSlotFwdOut, ctx->rank, P, step, stream));
     }
     {  // 5. all owners' rows are in: copy into the caller's out
       Phase ph(ctx, UA_PHASE_UNPACK_FWD, stream);
       UA_CUDA(ua::launch_wait_copy(static_cast<const int64_t*>(ctx->flags.local), kSlotFwdOut, P, step,
-                                   ctx->fwd_out.local, out, int64_t(S), stream));
+                                   ctx->fwd_out.local, out, int64_t(S), ctx->peer_err, stream));
       ctx->a2a_calls += 1;
       ctx->a2a_bytes += int64_t(P - 1) * int64_t(s.chunk()) * 2;
     }
@@ -596,14 +673,9 @@ ua_status ua_ulysses_attn_fwd(ua_ctx* ctx, const void* q, const void* k, const v
     ctx->a2a_calls += 1;
   }
   // 3. attention on the head shard, layout [N][B][Hl][D]; O straight into the send layout of #2
-  const int64_t sn = B * int64_t(s.Hl) * D, sh = D, sb = int64_t(s.Hl) * D;
   void* o_head = ws + plan.o_head;
-  ua::ViewArg o{o_head, sn, sh, sb};
-  {
-    Phase ph(ctx, UA_PHASE_ATTN_FWD, stream);
-    UA_TRY(launch_attention_fwd(recv[0], recv[1], recv[2], sn, sh, sb, o, nullptr, 0, 0, 0, lse, N,
-                                int64_t(s.Hl) * N, B, N, s.Hl, D, 0, N, stream));
-  }
+  UA_TRY(head_fwd(ctx, recv[0], recv[1], recv[2], head_layout(B, s.Hl, D), o_head, nullptr, lse, B, N, s.Hl, D,
+                  stream));
   void* recv_o = ws + plan.send;
   {  // 4. all-to-all #2: token block i of every local head goes back to rank i
     Phase ph(ctx, UA_PHASE_A2A_FWD_OUT, stream);
@@ -638,30 +710,15 @@ ua_status ua_ulysses_attn_bwd(ua_ctx* ctx, const void* q, const void* k, const v
   UA_TRY(check_device());
   UA_TRY(check_async(ctx));
   char* ws = static_cast<char*>(workspace);
-  const int64_t n_pad = (N + 127) / 128 * 128;
-  const float scale = float(1.0 / std::sqrt(double(D)));
 
   if (P == 1) {
     float* delta = reinterpret_cast<float*>(ws + plan.delta);
-    float* dq_acc = reinterpret_cast<float*>(ws + plan.dq_acc);
     {  // Delta[n][b][h] = sum_d dO.O (fp32)
       Phase ph(ctx, UA_PHASE_PACK_BWD, stream);
       UA_CUDA(ua::launch_pack(nullptr, nullptr, 0, B, N, H, D, 1, dout, out, delta, stream));
     }
-    const int64_t sn = int64_t(H) * D, sh = D, sb = N * H * D;
-    ua::ViewArg vdk{dk, sn, sh, sb}, vdv{dv, sn, sh, sb}, vdq{dq, sn, sh, sb};
-    {
-      Phase ph(ctx, UA_PHASE_ATTN_BWD, stream);
-      UA_CUDA(cudaMemsetAsync(dq_acc, 0, size_t(B * H * n_pad * D) * 4, stream));
-      UA_TRY(launch_attention_bwd(q, k, v, dout, sn, sh, sb, vdk, vdv, dq_acc, lse, N, int64_t(H) * N, delta,
-                                  B * int64_t(H), 1, H, B, N, H, D, reinterpret_cast<float2*>(ws + plan.lsed),
-                                  ctx->deterministic, stream));
-    }
-    {
-      Phase ph(ctx, UA_PHASE_DQ_FINALIZE, stream);
-      UA_CUDA(ua::launch_dq_finalize(dq_acc, vdq, B, N, H, D, scale, stream));
-    }
-    return UA_OK;
+    return head_bwd(ctx, q, k, v, dout, Strides{int64_t(H) * D, D, N * H * D}, lse, delta, dq, dk, dv, nullptr, B, N,
+                    H, D, ctx->deterministic, ws + plan.head, stream);
   }
 
   if (ctx->a2a_mode == UA_A2A_PEER) {
@@ -686,35 +743,26 @@ ua_status ua_ulysses_attn_bwd(ua_ctx* ctx, const void* q, const void* k, const v
     {
       Phase ph(ctx, UA_PHASE_A2A_BWD_IN, stream);
       UA_CUDA(ua::launch_wait_copy(static_cast<const int64_t*>(ctx->flags.local), kSlotBwdIn, P, step, nullptr,
-                                   nullptr, 0, stream));
+                                   nullptr, 0, ctx->peer_err, stream));
       ctx->a2a_calls += 1;
       ctx->a2a_bytes += int64_t(P - 1) * (int64_t(s.chunk()) * 2 * 4 + int64_t(s.Nl * B * s.Hl) * 4);
     }
     char* rin = static_cast<char*>(ctx->bwd_in.local);
     const float* rdelta = reinterpret_cast<const float*>(rin + 4 * S);
-    float* dq_acc = reinterpret_cast<float*>(ws + plan.dq_acc);
-    const int64_t sn = B * int64_t(s.Hl) * D, sh = D, sb = int64_t(s.Hl) * D;
-    const ua::PeerOut pdq = peer_out(ctx->bwd_out, 0, s, ctx->rank);
-    const ua::PeerOut pdk = peer_out(ctx->bwd_out, S, s, ctx->rank);
-    const ua::PeerOut pdv = peer_out(ctx->bwd_out, 2 * S, s, ctx->rank);
-    {  // 3. attention backward; dK, dV rows go straight to the token owners
-      Phase ph(ctx, UA_PHASE_ATTN_BWD, stream);
-      UA_CUDA(cudaMemsetAsync(dq_acc, 0, size_t(B * s.Hl * n_pad * D) * 4, stream));
-      ua::ViewArg none{nullptr, 0, 0, 0};
-      UA_TRY(launch_attention_bwd(rin, rin + S, rin + 2 * S, rin + 3 * S, sn, sh, sb, none, none, dq_acc, lse, N,
-                                  int64_t(s.Hl) * N, rdelta, B * int64_t(s.Hl), 1, s.Hl, B, N, s.Hl, D,
-                                  reinterpret_cast<float2*>(ws + plan.lsed), ctx->deterministic, stream, &pdk, &pdv));
-    }
-    {  // 4. dq = bf16(scale * dq_acc) into the token owners' buffers, then flag
-      Phase ph(ctx, UA_PHASE_DQ_FINALIZE, stream);
-      UA_CUDA(ua::launch_finalize_push(dq_acc, pdq, B, N, s.Hl, D, scale, stream));
+    const ua::PeerOut owners[3] = {peer_out(ctx->bwd_out, 0, s, ctx->rank), peer_out(ctx->bwd_out, S, s, ctx->rank),
+                                   peer_out(ctx->bwd_out, 2 * S, s, ctx->rank)};
+    // 3+4. attention backward; dK, dV rows (epilogue) and dQ rows (finaliser) go straight to the token owners
+    UA_TRY(head_bwd(ctx, rin, rin + S, rin + 2 * S, rin + 3 * S, head_layout(B, s.Hl, D), lse, rdelta, nullptr,
+                    nullptr, nullptr, owners, B, N, s.Hl, D, ctx->deterministic, ws + plan.head, stream));
+    {
+      Phase ph(ctx, UA_PHASE_A2A_BWD_OUT, stream);
       UA_CUDA(ua::launch_signal(fl, kSlotBwdOut, ctx->rank, P, step, stream));
     }
     {  // 5. all heads' rows are in: copy into the caller's dq, dk, dv
       Phase ph(ctx, UA_PHASE_UNPACK_BWD, stream);
       char* rout = static_cast<char*>(ctx->bwd_out.local);
       UA_CUDA(ua::launch_wait_copy(static_cast<const int64_t*>(ctx->flags.local), kSlotBwdOut, P, step, rout, dq,
-                                   int64_t(S), stream));
+                                   int64_t(S), ctx->peer_err, stream));
       UA_CUDA(cudaMemcpyAsync(dk, rout + S, S, cudaMemcpyDeviceToDevice, stream));
       UA_CUDA(cudaMemcpyAsync(dv, rout + 2 * S, S, cudaMemcpyDeviceToDevice, stream));
       ctx->a2a_calls += 1;
@@ -728,7 +776,6 @@ ua_status ua_ulysses_attn_bwd(ua_ctx* ctx, const void* q, const void* k, const v
   void* recv[4] = {ws + plan.recv, ws + plan.recv + S, ws + plan.recv + 2 * S, ws + plan.recv + 3 * S};
   float* send_delta = reinterpret_cast<float*>(ws + plan.send_delta);
   float* recv_delta = reinterpret_cast<float*>(ws + plan.recv_delta);
-  float* dq_acc = reinterpret_cast<float*>(ws + plan.dq_acc);
   void* grad[3] = {ws + plan.grad, ws + plan.grad + S, ws + plan.grad + 2 * S};
   const void* src[4] = {q, k, v, dout};
   {  // 1. pack q, k, v, dO + Delta = rowsum(dO * O) in sequence space
@@ -747,20 +794,9 @@ ua_status ua_ulysses_attn_bwd(ua_ctx* ctx, const void* q, const void* k, const v
     UA_NCCL(ncclGroupEnd());
     ctx->a2a_calls += 1;
   }
-  // 3. attention backward on the head shard [N][B][Hl][D]
-  const int64_t sn = B * int64_t(s.Hl) * D, sh = D, sb = int64_t(s.Hl) * D;
-  ua::ViewArg vdq{grad[0], sn, sh, sb}, vdk{grad[1], sn, sh, sb}, vdv{grad[2], sn, sh, sb};
-  {
-    Phase ph(ctx, UA_PHASE_ATTN_BWD, stream);
-    UA_CUDA(cudaMemsetAsync(dq_acc, 0, size_t(B * s.Hl * n_pad * D) * 4, stream));
-    UA_TRY(launch_attention_bwd(recv[0], recv[1], recv[2], recv[3], sn, sh, sb, vdk, vdv, dq_acc, lse, N,
-                                int64_t(s.Hl) * N, recv_delta, B * int64_t(s.Hl), 1, s.Hl, B, N, s.Hl, D,
-                                reinterpret_cast<float2*>(ws + plan.lsed), ctx->deterministic, stream));
-  }
-  {
-    Phase ph(ctx, UA_PHASE_DQ_FINALIZE, stream);
-    UA_CUDA(ua::launch_dq_finalize(dq_acc, vdq, B, N, s.Hl, D, scale, stream));
-  }
+  // 3+4. attention backward on the head shard [N][B][Hl][D]; dq, dk, dv into the send layout of #4
+  UA_TRY(head_bwd(ctx, recv[0], recv[1], recv[2], recv[3], head_layout(B, s.Hl, D), lse, recv_delta, grad[0], grad[1],
+                  grad[2], nullptr, B, N, s.Hl, D, ctx->deterministic, ws + plan.head, stream));
   void* rgrad[3] = {ws + plan.send, ws + plan.send + S, ws + plan.send + 2 * S};
   {  // 4. all-to-all #4 (fused dq, dk, dv) back to the token owners
     Phase ph(ctx, UA_PHASE_A2A_BWD_OUT, stream);
@@ -774,6 +810,127 @@ ua_status ua_ulysses_attn_bwd(ua_ctx* ctx, const void* q, const void* k, const v
     UA_CUDA(ua::launch_unpack(usrc, udst, 3, B, s.Nl, H, D, P, stream));
   }
   return UA_OK;
+}
+
+// ------------------------------------------------------------ rank-local steps (no communication)
+ua_status ua_pack_seq_to_head(const void* const* src, void* const* dst, int ntensors, int64_t B, int64_t N, int H,
+                              int D, int P, const void* dout, const void* out, float* delta, ua_stream_t stream) {
+  UA_TRY(ua_validate(B, N, H, D, P));
+  const bool with_delta = dout || out || delta;
+  if (ntensors < 0 || ntensors > 4 || (ntensors == 0 && !with_delta))
+    return fail(UA_ERR_INVALID_ARG, "ntensors=%d (0..4; 0 only with Delta)", ntensors);
+  if (ntensors > 0 && (!src || !dst)) return fail(UA_ERR_INVALID_ARG, "src / dst arrays are NULL");
+  for (int w = 0; w < ntensors; ++w) UA_TRY(check_ptrs({src[w], dst[w]}));
+  if (with_delta) UA_TRY(check_ptrs({dout, out, delta}));
+  UA_TRY(check_device());
+  UA_TRY(check_async(nullptr));
+  UA_CUDA(ua::launch_pack(src, dst, ntensors, B, N / P, H, D, P, dout, out, delta,
+                          reinterpret_cast<cudaStream_t>(stream)));
+  return UA_OK;
+}
+
+ua_status ua_unpack_head_to_seq(const void* const* src, void* const* dst, int ntensors, int64_t B, int64_t N, int H,
+                                int D, int P, ua_stream_t stream) {
+  UA_TRY(ua_validate(B, N, H, D, P));
+  if (ntensors < 1 || ntensors > 4 || !src || !dst) return fail(UA_ERR_INVALID_ARG, "ntensors=%d (1..4)", ntensors);
+  for (int w = 0; w < ntensors; ++w) UA_TRY(check_ptrs({src[w], dst[w]}));
+  UA_TRY(check_device());
+  UA_TRY(check_async(nullptr));
+  UA_CUDA(ua::launch_unpack(src, dst, ntensors, B, N / P, H, D, P, reinterpret_cast<cudaStream_t>(stream)));
+  return UA_OK;
+}
+
+ua_status ua_push_seq_to_head(const void* const* src, int ntensors, void* const* dst_rank, int64_t B, int64_t N, int H,
+                              int D, int P, int rank, const void* dout, const void* out, ua_stream_t stream) {
+  UA_TRY(ua_validate(B, N, H, D, P));
+  if (P > ua::kMaxPeers) return fail(UA_ERR_UNSUPPORTED, "P=%d > %d", P, ua::kMaxPeers);
+  if (rank < 0 || rank >= P) return fail(UA_ERR_INVALID_ARG, "rank=%d not in [0, %d)", rank, P);
+  if (ntensors < 1 || ntensors > 4 || !src || !dst_rank)
+    return fail(UA_ERR_INVALID_ARG, "ntensors=%d (1..4)", ntensors);
+  if ((dout == nullptr) != (out == nullptr)) return fail(UA_ERR_INVALID_ARG, "dout and out: both or neither");
+  ua::PeerPack pk{};
+  for (int w = 0; w < ntensors; ++w) {
+    UA_TRY(check_ptrs({src[w]}));
+    pk.src[w] = src[w];
+  }
+  for (int j = 0; j < P; ++j) {
+    UA_TRY(check_ptrs({dst_rank[j]}));
+    pk.dst[j] = dst_rank[j];
+  }
+  if (dout) UA_TRY(check_ptrs({dout, out}));
+  pk.ntensors = ntensors;
+  pk.dout = dout;
+  pk.out = out;
+  UA_TRY(check_device());
+  UA_TRY(check_async(nullptr));
+  UA_CUDA(ua::launch_pack_push(pk, B, N / P, H, D, P, rank, reinterpret_cast<cudaStream_t>(stream)));
+  return UA_OK;
+}
+
+namespace {
+// Owner maps of the token-owner tensors [B][N/P][H][D] (o_owner[i] = rank i's tensor).
+ua_status owner_map(void* const* owners, const Shape& s, int rank, ua::PeerOut* o) {
+  if (s.P > ua::kMaxPeers) return fail(UA_ERR_UNSUPPORTED, "P=%d > %d", s.P, ua::kMaxPeers);
+  *o = ua::PeerOut{};
+  for (int i = 0; i < s.P; ++i) {
+    UA_TRY(check_ptrs({owners[i]}));
+    o->base[i] = owners[i];
+  }
+  o->nl = s.Nl;
+  o->H = s.H;
+  o->h0 = rank * s.Hl;
+  return UA_OK;
+}
+}  // namespace
+
+ua_status ua_head_attn_fwd(const void* q, const void* k, const void* v, void* o, float* lse, int64_t B, int64_t N,
+                           int H, int D, int P, int rank, void* const* o_owner, ua_stream_t stream) {
+  UA_TRY(ua_validate(B, N, H, D, P));
+  if (rank < 0 || rank >= P) return fail(UA_ERR_INVALID_ARG, "rank=%d not in [0, %d)", rank, P);
+  UA_TRY(check_ptrs({q, k, v, lse}));
+  const Shape s = make_shape(B, N, H, D, P);
+  ua::PeerOut po;
+  if (o_owner) {
+    if (o) return fail(UA_ERR_INVALID_ARG, "o must be NULL when o_owner is given");
+    UA_TRY(owner_map(o_owner, s, rank, &po));
+  } else {
+    UA_TRY(check_ptrs({o}));
+  }
+  UA_TRY(check_device());
+  UA_TRY(check_async(nullptr));
+  return head_fwd(nullptr, q, k, v, head_layout(B, s.Hl, D), o, o_owner ? &po : nullptr, lse, B, N, s.Hl, D,
+                  reinterpret_cast<cudaStream_t>(stream));
+}
+
+ua_status ua_head_attn_bwd_workspace_size(int64_t B, int64_t N, int H, int D, int P, size_t* bytes) {
+  UA_TRY(ua_validate(B, N, H, D, P));
+  if (!bytes) return fail(UA_ERR_INVALID_ARG, "bytes is NULL");
+  *bytes = head_bwd_bytes(make_shape(B, N, H, D, P));
+  return UA_OK;
+}
+
+ua_status ua_head_attn_bwd(const void* q, const void* k, const void* v, const void* dout, const float* lse,
+                           const float* delta, void* dq, void* dk, void* dv, int64_t B, int64_t N, int H, int D, int P,
+                           int rank, void* const* owners, int deterministic, void* workspace, size_t workspace_bytes,
+                           ua_stream_t stream) {
+  UA_TRY(ua_validate(B, N, H, D, P));
+  if (rank < 0 || rank >= P) return fail(UA_ERR_INVALID_ARG, "rank=%d not in [0, %d)", rank, P);
+  UA_TRY(check_ptrs({q, k, v, dout, lse, delta, workspace}));
+  const Shape s = make_shape(B, N, H, D, P);
+  if (workspace_bytes < head_bwd_bytes(s))
+    return fail(UA_ERR_INVALID_ARG, "workspace too small: need %zu bytes, got %zu", head_bwd_bytes(s),
+                workspace_bytes);
+  ua::PeerOut po[3];
+  if (owners) {
+    if (dq || dk || dv) return fail(UA_ERR_INVALID_ARG, "dq, dk, dv must be NULL when owners are given");
+    for (int w = 0; w < 3; ++w) UA_TRY(owner_map(owners + w * P, s, rank, &po[w]));
+  } else {
+    UA_TRY(check_ptrs({dq, dk, dv}));
+  }
+  UA_TRY(check_device());
+  UA_TRY(check_async(nullptr));
+  return head_bwd(nullptr, q, k, v, dout, head_layout(B, s.Hl, D), lse, delta, dq, dk, dv, owners ? po : nullptr, B, N,
+                  s.Hl, D, deterministic ? 1 : 0, static_cast<char*>(workspace), reinterpret_cast<cudaStream_t>(stream));
 }
 
 // ------------------------------------------------------------ LSS sequence parallelism

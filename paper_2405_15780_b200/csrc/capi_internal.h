@@ -38,6 +38,10 @@ struct ua_ctx {
     void* peer[ua::kMaxPeers] = {};
   };
   PeerBuf flags, fwd_in, fwd_out, bwd_in, bwd_out;
+  // Host-mapped error word of the bounded peer waits (peer.cu wait_copy_kernel):
+  // peer_err_host != 0 after a wait timed out; peer_err is its device alias.
+  int* peer_err_host = nullptr;
+  int* peer_err = nullptr;
   void* lt = nullptr;  // cublasLtHandle_t of the projection layer (layer.cpp), created on first use
   int64_t step_fwd = 0, step_bwd = 0;
   cudaEvent_t get_event() {

@@ -253,13 +253,8 @@ __global__ void __launch_bounds__(BwdDqCfg<D>::kThreads, 1) attn_bwd_dq_kernel(c
 template <int D>
 cudaError_t launch_bwd_dq_impl(const BwdParams& p, cudaStream_t stream) {
   using C = BwdDqCfg<D>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(attn_bwd_dq_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         C::kSmemBytes);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  cudaError_t e = set_max_smem(attn_bwd_dq_kernel<D>, C::kSmemBytes);
+  if (e != cudaSuccess) return e;
   dim3 grid((p.n + 127) / 128, p.heads, p.batch);
   attn_bwd_dq_kernel<D><<<grid, C::kThreads, C::kSmemBytes, stream>>>(p);
   return cudaGetLastError();

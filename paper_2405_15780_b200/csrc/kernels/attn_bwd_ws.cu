@@ -1,7 +1,7 @@
 // attn_bwd_ws.cu — persistent, warp-specialised attention backward (sm_100a),
 // D in {32, 64, 80 (= head dim 72 padded), 128}.
 //
-// Mathematics as attn_bwd.cu:
+// Mathematics (FlashAttention-2's recompute backward):
 //   P = exp(S - lse), dV += P^T dO, dS = P (dP - Delta), dK += scale dS^T Q,
 //   dQ += scale dS K   (dQ partials reduced in fp32; scale applied later).
 //
@@ -737,15 +737,10 @@ __global__ void __launch_bounds__(ws_threads<D, kDq>(), 1) attn_bwd_ws_kernel(co
 template <int D, bool kDq>
 cudaError_t launch_bwd_ws_impl(const BwdParams& p, cudaStream_t stream) {
   using C = BwdWsCfg<D>;
-  static int num_sms = 0;
-  if (num_sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaError_t e =
-        cudaFuncSetAttribute(attn_bwd_ws_kernel<D, kDq>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
-    if (e != cudaSuccess) return e;
-  }
+  const int num_sms = current_num_sms();
+  if (num_sms <= 0) return cudaErrorNoDevice;
+  cudaError_t e = set_max_smem(attn_bwd_ws_kernel<D, kDq>, C::kSmemBytes);
+  if (e != cudaSuccess) return e;
   const int64_t items = int64_t(p.batch) * p.heads * ((p.n_kv + 127) / 128);
   const int grid = int(items < num_sms ? items : num_sms);
 #if UA_TRACE

@@ -335,13 +335,8 @@ __global__ void __launch_bounds__(640, 1) attn_fwd_split_kernel(const __grid_con
 template <int D>
 cudaError_t launch_split_impl(const FwdParams& p, int B, int Hx, cudaStream_t stream) {
   using C = SplitCfg<D>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e =
-        cudaFuncSetAttribute(attn_fwd_split_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  cudaError_t e = set_max_smem(attn_fwd_split_kernel<D>, C::kSmemBytes);
+  if (e != cudaSuccess) return e;
   dim3 grid((p.n_q + 255) / 256, Hx, B);
   attn_fwd_split_kernel<D><<<grid, C::kThreads, C::kSmemBytes, stream>>>(p);
   return cudaGetLastError();

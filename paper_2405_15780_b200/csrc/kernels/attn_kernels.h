@@ -78,10 +78,26 @@ struct alignas(64) BwdParams {
   int deterministic;  // 1: dQ by the query-stationary kernel, stored (not reduce-added) into dq_acc
 };
 
+// Launch setup that is correct in a process driving several GPUs: the dynamic
+// shared-memory opt-in is a per-device function attribute, so launchers set it
+// on every launch (a cheap driver call) instead of caching it process-wide, and
+// persistent grids are sized from the current device's SM count.
+template <class Kernel>
+inline cudaError_t set_max_smem(Kernel kernel, int bytes) {
+  return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
+inline int current_num_sms() {
+  int dev = 0, n = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+    return 0;
+  return n;
+}
+
 cudaError_t launch_attn_fwd(const FwdParams& p, int D, int B, int heads, cudaStream_t stream);
 // D <= 64 column-split forward (attn_fwd_split.cu); launch_attn_fwd dispatches to it when enabled.
 cudaError_t launch_attn_fwd_split(const FwdParams& p, int D, int B, int heads, cudaStream_t stream);
-cudaError_t launch_attn_bwd(const BwdParams& p, int D, int B, int heads, cudaStream_t stream);
+// The backward (attn_bwd_ws.cu): persistent KV-stationary kernel (+ the query-stationary dQ kernel
+// in deterministic mode).
 cudaError_t launch_attn_bwd_ws(const BwdParams& p, int D, cudaStream_t stream);
 // Deterministic dQ (attn_bwd_dq.cu): query-stationary, dq_acc rows = sum_j dS_ij k_j (unscaled, fp32,
 // plain stores, fixed key order).  Called by launch_attn_bwd_ws when p.deterministic.
@@ -92,7 +108,7 @@ cudaError_t launch_attn_bwd_dq(const BwdParams& p, int D, cudaStream_t stream);
 //   src[w]  : [B][Nl][H][D]          (rank-local sequence shard, user layout)
 //   dst[w]  : [P][Nl][B][Hl][D]      (chunk j = heads j*Hl.. of every token)
 // If delta_dst != nullptr, also Delta[b,t,h] = sum_d dO.O in fp32 from
-// (dout, out) [B][Nl][H][D] into delta_dst [P][Nl][B][Hl] (P == 1: [B][H][Nl]).
+// (dout, out) [B][Nl][H][D] into delta_dst [P][Nl][B][Hl] (P == 1: [Nl][B][H]).
 cudaError_t launch_pack(const void* const* src, void* const* dst, int ntensors, int64_t B, int64_t Nl, int H, int D,
                         int P, const void* dout, const void* out, float* delta_dst, cudaStream_t stream);
 // Received head chunks -> sequence shard, for `ntensors` tensors:
@@ -112,8 +128,9 @@ cudaError_t launch_bwd_prep(const float* lse, int64_t l_sh, int64_t l_sb, const 
 cudaError_t launch_pack_push(const PeerPack& pk, int64_t B, int64_t Nl, int H, int D, int P, int rank,
                              cudaStream_t stream);
 cudaError_t launch_signal(const PeerFlags& f, int slot, int rank, int P, int64_t step, cudaStream_t stream);
+// Spins (bounded: 60 s, then sets *err = 1 and skips the copy) until every peer's flag reached step.
 cudaError_t launch_wait_copy(const int64_t* flags, int slot, int P, int64_t step, const void* src, void* dst,
-                             int64_t bytes, cudaStream_t stream);
+                             int64_t bytes, int* err, cudaStream_t stream);
 cudaError_t launch_finalize_push(const float* dq_acc, const PeerOut& o, int64_t B, int64_t N, int heads, int D,
                                  float scale, cudaStream_t stream);
 // Exact merge of two LSS segment results (in place into a):

@@ -84,15 +84,37 @@ __global__ void signal_kernel(PeerFlags f, int slot, int rank, int P, int64_t st
   if (p < P) st_release_sys(f.peer[p] + slot * kMaxPeers + rank, step);
 }
 
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// A peer that never raises its flag (it failed validation, died, or diverged)
+// must not hang this GPU: after kPeerWaitNs the wait gives up, records the
+// timeout in the ctx's host-mapped error word and skips its copy; the next
+// library call on that ctx returns UA_ERR_CUDA.
+constexpr uint64_t kPeerWaitNs = 60ull * 1000 * 1000 * 1000;
+
 __global__ void __launch_bounds__(256) wait_copy_kernel(const int64_t* flags, int slot, int P, int64_t step,
                                                         const uint4* __restrict__ src, uint4* __restrict__ dst,
-                                                        int64_t n_vec) {
+                                                        int64_t n_vec, volatile int* err) {
+  __shared__ int timed_out;
+  if (threadIdx.x == 0) timed_out = 0;
+  __syncthreads();
   if (threadIdx.x < P) {
     const int64_t* f = flags + slot * kMaxPeers + threadIdx.x;
+    const uint64_t t0 = globaltimer_ns();
     while (ld_acquire_sys(f) < step) {
+      if (globaltimer_ns() - t0 > kPeerWaitNs) {
+        timed_out = 1;
+        if (err != nullptr) *err = 1;
+        break;
+      }
     }
   }
   __syncthreads();
+  if (timed_out) return;
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n_vec; i += int64_t(gridDim.x) * blockDim.x)
     dst[i] = src[i];
 }
@@ -190,10 +212,10 @@ cudaError_t launch_signal(const PeerFlags& f, int slot, int rank, int P, int64_t
 }
 
 cudaError_t launch_wait_copy(const int64_t* flags, int slot, int P, int64_t step, const void* src, void* dst,
-                             int64_t bytes, cudaStream_t stream) {
+                             int64_t bytes, int* err, cudaStream_t stream) {
   const int64_t n_vec = bytes / 16;
   wait_copy_kernel<<<n_vec > 0 ? grid_for(n_vec, 256) : 1, 256, 0, stream>>>(
-      flags, slot, P, step, static_cast<const uint4*>(src), static_cast<uint4*>(dst), n_vec);
+      flags, slot, P, step, static_cast<const uint4*>(src), static_cast<uint4*>(dst), n_vec, err);
   return cudaGetLastError();
 }
 

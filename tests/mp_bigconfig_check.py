@@ -8,8 +8,10 @@ checks against the fp64 oracle what the oracle can compute row by row:
     both sides of every shard boundary, random rows) for two heads that live on
     different ranks after the all-to-all (head 0 and head H-1);
   * dQ at the same sampled rows (oracle.attn_bwd_dq_rows, exact per row);
-  * dK / dV through invariants that hold at any size, per head, reduced over
-    ranks: sum_j dK_j = 0, sum_j dV_j = sum_i dO_i, <Q, dQ> = <K, dK>;
+  * dK / dV at the same sampled KEY rows of head 0, exact per row
+    (oracle.attn_bwd_kv_rows; c3 and c4), and through invariants that hold at
+    any size, per head, reduced over ranks: sum_j dK_j = 0,
+    sum_j dV_j = sum_i dO_i, <Q, dQ> = <K, dK>;
   * everything finite; a2a call law (2 + 2).
 Prints "BIG_OK" on rank 0 on success."""
 import argparse
@@ -88,6 +90,26 @@ def main():
             gi = np.array(rows) + rank * Nl
             sel = bh[:, 1] == hi
             gate_lse(lse_np[0, h - rank * hl, gi], l_ref[sel])
+
+    # ---- dK / dV at sampled KEY rows of head 0, element by element (c3, c4: the oracle
+    # recomputes that head's lse / Delta in a few minutes; c5 is out of its reach)
+    if N <= 200000:
+        keys_local = np.array(rows)
+        local = dict(keys=(keys_local + rank * Nl).tolist(),
+                     dk=dk[0, torch.from_numpy(keys_local).to(dev), 0].float().cpu().numpy(),
+                     dv=dv[0, torch.from_numpy(keys_local).to(dev), 0].float().cpu().numpy())
+        allr = [None] * P
+        dist.all_gather_object(allr, local)
+        if rank == 0:
+            keys = np.concatenate([np.array(x["keys"]) for x in allr])
+            got_k = np.concatenate([x["dk"] for x in allr])
+            got_v = np.concatenate([x["dv"] for x in allr])
+            oracle.set_num_threads(len(os.sched_getaffinity(0)))  # torchrun sets OMP_NUM_THREADS=1
+            h0 = [synth.to_f64(synth.normal_bf16(B, N, H, D, seed, nm, heads=[0]))[0, :, 0] for nm in ("q", "k", "v", "do")]
+            dk_ref, dv_ref = oracle.attn_bwd_kv_rows(*h0, keys)
+            gate_grad(got_k, dk_ref)
+            gate_grad(got_v, dv_ref)
+        dist.barrier()
 
     # ---- dK / dV invariants, per head, summed over ranks
     qd, kd, dod = (x.to(torch.float64) for x in (qs, ks, ds))

@@ -138,3 +138,41 @@ def test_ctx_mode_setters_validate_arguments():
     assert L.ua_ctx_get_deterministic(None, ctypes.byref(ctypes.c_int(0))) == 1
     assert L.ua_ctx_set_a2a_mode(None, 0) == 1
     assert "ctx" in L.ua_last_error().decode()
+
+
+def test_rank_local_steps_validate_before_any_launch():
+    """The rank-local step entry points check shapes (the same codes as
+    ua_validate) and pointers on the host before touching the device."""
+    import ctypes
+    L = ua.lib()
+    arr = (ctypes.c_void_p * 4)(16, 32, 48, 64)
+    # S:248 head limit (H=4, P=8) and S:244 N % P, before anything else
+    assert L.ua_pack_seq_to_head(arr, arr, 1, 1, 16, 4, 64, 8, None, None, None, None) == 2
+    assert L.ua_unpack_head_to_seq(arr, arr, 1, 1, 10, 4, 64, 4, None) == 3
+    assert L.ua_head_attn_fwd(None, None, None, None, None, 1, 16, 4, 64, 8, 0, None, None) == 2
+    # bad counts / ranks / pointers
+    assert L.ua_pack_seq_to_head(arr, arr, 5, 1, 16, 4, 64, 2, None, None, None, None) == 1
+    assert L.ua_pack_seq_to_head(arr, arr, 0, 1, 16, 4, 64, 2, None, None, None, None) == 1   # 0 tensors, no Delta
+    assert L.ua_unpack_head_to_seq(arr, arr, 0, 1, 16, 4, 64, 2, None) == 1
+    assert L.ua_push_seq_to_head(arr, 1, arr, 1, 16, 4, 64, 2, 2, None, None, None) == 1      # rank >= P
+    assert L.ua_head_attn_fwd(None, None, None, None, None, 1, 16, 4, 64, 2, 0, None, None) == 1
+    assert L.ua_head_attn_fwd(*(ctypes.c_void_p(16),) * 5, 1, 16, 4, 64, 2, 3, None, None) == 1  # rank >= P
+    assert L.ua_head_attn_bwd(*(ctypes.c_void_p(16),) * 9, 1, 16, 4, 64, 2, 0, None, 0, ctypes.c_void_p(16), 0,
+                              None) == 1                                                      # workspace too small
+    misaligned = (ctypes.c_void_p * 1)(18)
+    assert L.ua_unpack_head_to_seq(misaligned, arr, 1, 1, 16, 4, 64, 2, None) == 1
+
+
+def test_head_attn_bwd_workspace_size():
+    """fp32 dQ accumulator [B*Hl][N_pad][D] + (lse, Delta) table [B*Hl][N_pad] float2."""
+    import ctypes
+    n = ctypes.c_size_t(0)
+    B, N, H, D, P = 2, 1000, 8, 64, 4
+    assert ua.lib().ua_head_attn_bwd_workspace_size(B, N, H, D, P, ctypes.byref(n)) == 0
+    n_pad = 1024
+    need = B * (H // P) * n_pad * (D * 4 + 8)
+    assert need <= n.value <= need + 512
+    # the P = 1 backward's workspace holds Delta plus exactly this region
+    _, b1 = ua.workspace_size(B, N, H, D, 1)
+    assert ua.lib().ua_head_attn_bwd_workspace_size(B, N, H, D, 1, ctypes.byref(n)) == 0
+    assert b1 >= n.value + B * N * H * 4

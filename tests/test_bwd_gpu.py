@@ -26,6 +26,15 @@ def ctx(ua):
     c.close()
 
 
+@pytest.fixture(scope="module")
+def dctx(ua):
+    c = ua.Context(P=1)
+    c.set_deterministic(True)
+    assert c.deterministic()
+    yield c
+    c.close()
+
+
 def run_fwd_bwd(ua, ctx, q, k, v, do):
     qc, kc, vc, dc = (t.cuda() for t in (q, k, v, do))
     r = ua.ulysses_attn_fwd(ctx, qc, kc, vc)
@@ -58,6 +67,9 @@ def check(ua, ctx, B, N, H, D, sigma, seed):
     (300, 2, 72, 1.0),      # D=72 (ViT-10B)
     (1000, 3, 72, 2.0),
     (129, 2, 72, 1.0),
+    (1000, 2, 64, 4.0),     # sigma_qk = 4: row maxima move by >> 2^8, the lazy rescale fires on most tiles
+    (2048, 2, 128, 4.0),
+    (777, 2, 32, 4.0),
 ])
 def test_bwd_parity_small(ua, ctx, N, H, D, sigma):
     check(ua, ctx, 1, N, H, D, sigma, seed=100 + N)
@@ -79,6 +91,53 @@ def test_bwd_parity_c2(ua, ctx, sigma):
     dq, dk, dv, _, _, gabs = oracle.attn_bwd(*sub, with_abs=True)
     for g, ref, a in zip(got, (dq, dk, dv), gabs):
         gate_grad(g[:, :, heads], ref, gate_a=sigma == 1.0, gabs=a)
+
+
+@pytest.mark.parametrize("det", [False, True])
+@pytest.mark.parametrize("N,H,D,heads", [(8192, 16, 32, [0, 15]), (8192, 8, 72, [3, 7])])
+def test_bwd_more_items_than_sms(ua, ctx, dctx, N, H, D, heads, det):
+    """D = 32 (1,024 work items) and D = 72 (512 items) on 148 SMs: every CTA of
+    the persistent backward runs several items, so the cross-item hand-offs
+    (K/V reload, TMEM accumulator reuse, DQ_LATE issue order) are exercised at
+    these head dims too.  Oracle on a subset of the heads."""
+    q, k, v, do = synth.qkv(1, N, H, D, seed=900 + D, with_do=True)
+    got = run_fwd_bwd(ua, dctx if det else ctx, q, k, v, do)
+    sub = [synth.to_f64(t)[:, :, heads] for t in (q, k, v, do)]
+    dq, dk, dv, _, _, gabs = oracle.attn_bwd(*sub, with_abs=True)
+    for g, ref, a in zip(got, (dq, dk, dv), gabs):
+        gate_grad(g[:, :, heads], ref, gate_a=True, gabs=a)
+
+
+def sample_rows(N, rng, extra=12):
+    """Both ends, both sides of 128-row tile boundaries near the ends and the
+    middle, the boundary of the persistent grid's first item wave (148 key
+    tiles), and random rows."""
+    fixed = [0, 1, 127, 128, 129, 255, 256, 148 * 128 - 1, 148 * 128, N // 2 - 1, N // 2, N - 129, N - 128, N - 2,
+             N - 1]
+    return np.unique(np.array([r for r in fixed if 0 <= r < N] + list(rng.integers(0, N, extra))))
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("cfg,head", [("c3", 9), ("c4", 17)])
+def test_bwd_full_size_sampled_rows(ua, ctx, cfg, head):
+    """Full-size backward at P = 1 (c3: N = 65,536, D = 128; c4: N = 188,416,
+    D = 64): exact fp64 dK, dV for sampled KEY rows of one head
+    (oracle.attn_bwd_kv_rows, which recomputes every lse_i and Delta_i) and dQ
+    for sampled query rows, element by element (Gate A + relL2 + elementwise)."""
+    c = synth.CONFIGS[cfg]
+    B, N, H, D = c["B"], c["N"], c["H"], c["D"]
+    q, k, v, do = synth.qkv(B, N, H, D, seed=synth.BASE_SEED, with_do=True)
+    dq, dk, dv = run_fwd_bwd(ua, ctx, q, k, v, do)
+    for t in (dq, dk, dv):
+        assert np.isfinite(t).all()
+    rows = sample_rows(N, np.random.default_rng(17))
+    qh, kh, vh, doh = (synth.to_f64(t[0, :, head]) for t in (q, k, v, do))
+    dk_ref, dv_ref = oracle.attn_bwd_kv_rows(qh, kh, vh, doh, rows)
+    gate_grad(dk[0, rows, head], dk_ref)
+    gate_grad(dv[0, rows, head], dv_ref)
+    bh = np.array([(0, 0)] * len(rows))
+    dq_ref = oracle.attn_bwd_dq_rows(qh[rows], doh[rows], bh, kh[None, :, None, :], vh[None, :, None, :])
+    gate_grad(dq[0, rows, head], dq_ref)
 
 
 def test_bwd_invariants(ua, ctx):
@@ -108,14 +167,6 @@ def test_bwd_deterministic_dkdv(ua, ctx):
 
 
 # ------------------------------------------------------------ deterministic mode
-@pytest.fixture(scope="module")
-def dctx(ua):
-    c = ua.Context(P=1)
-    c.set_deterministic(True)
-    assert c.deterministic()
-    yield c
-    c.close()
-
 
 @pytest.mark.parametrize("B,N,H,D,sigma", [
     (1, 256, 4, 32, 1.0),      # c1

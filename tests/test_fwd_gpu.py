@@ -46,6 +46,10 @@ def run_fwd(ua, ctx, q, k, v):
     (300, 2, 72, 1.0),      # D=72 (ViT-10B): padded 80-wide MMA tiles, SW32 atoms
     (1000, 3, 72, 2.0),
     (129, 2, 72, 1.0),
+    (1000, 2, 64, 4.0),     # sigma_qk = 4: row maxima move by >> 2^8, the lazy rescale fires on most tiles
+    (2048, 2, 128, 4.0),
+    (777, 2, 32, 4.0),
+    (300, 2, 72, 4.0),
 ])
 def test_fwd_parity_small(ua, ctx, N, H, D, sigma):
     q, k, v = synth.qkv(1, N, H, D, seed=7 + N, sigma_qk=sigma)
