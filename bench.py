@@ -45,6 +45,7 @@ PAPER_CONTEXT = {
     "cite": "PAPER.md P:425 (section 6.1)",
 }
 UNIT = "TFLOP/s"
+NVLINK_GBS = 900.0   # NVLink 5 per direction per GPU (B200_PROFILING.md / SURVEY §8(e))
 WORKLOAD = dict(name="c4", B=1, N=188416, H=32, D=64)
 # BASELINE.json configs by (N, H, D) (c1 is the oracle-sized parity case)
 CONFIG_NAMES = {(256, 4, 32): "c1", (8192, 16, 64): "c2", (65536, 16, 128): "c3", (188416, 32, 64): "c4",
@@ -133,6 +134,33 @@ def devices_in_use(P):
     return set(ids[:P]) if ids else set(range(P))
 
 
+def host_cpu():
+    """lscpu model name and the host's logical CPU count."""
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                model = line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return model, os.cpu_count()
+
+
+def load_ncu(kind, D, N, P, det=False):
+    """Pipe utilisations of the attention kernels from the committed ncu
+    summary (profiles/ncu_metrics.json, written from `ncu --set full`
+    captures; the file names its source reports)."""
+    path = os.path.join(ROOT, "profiles", "ncu_metrics.json")
+    if not os.path.exists(path):
+        return None
+    try:
+        d = json.load(open(path))
+        return d.get(f"{kind}{'_det' if det else ''}_D{D}_N{N}_P{P}")
+    except Exception:
+        return None
+
+
 def cpu_baseline(steps=1, n_sample=24576, D=64):
     """The fp64 oracle as it stands: fwd + bwd of one head over the first
     n_sample tokens (same D), timed on this host's cores."""
@@ -150,10 +178,16 @@ def cpu_baseline(steps=1, n_sample=24576, D=64):
         times.append(time.perf_counter() - t0)
     fwd, bwd = flops_per_step(1, n_sample, 1, D)
     t = float(np.mean(times))
-    return dict(value=(fwd + bwd) / t / 1e12, unit=UNIT, cores=oracle.num_threads(), kind="oracle",
+    value = (fwd + bwd) / t / 1e12
+    full_fwd, full_bwd = flops_per_step(WORKLOAD["B"], WORKLOAD["N"], WORKLOAD["H"], D)
+    model, ncpu = host_cpu()
+    return dict(value=value, unit=UNIT, cores=oracle.num_threads(), kind="oracle",
                 sample=f"fwd+bwd of 1 of {WORKLOAD['H']} heads over the first {n_sample} of {WORKLOAD['N']} tokens "
                        f"(D={D}), fp64 oracle, {steps} run(s) of {t:.2f} s; algorithmic flops 14*n^2*D per head",
-                seconds=t)
+                seconds=t, cpu_model=model, host_logical_cpus=ncpu, threads=oracle.num_threads(),
+                extrapolated_full_c4_s=(full_fwd + full_bwd) / (value * 1e12),
+                extrapolated_note="EXTRAPOLATED, not measured: full c4 fwd+bwd (14*N^2*H*D = "
+                                  f"{(full_fwd + full_bwd):.3e} flop) at the sampled rate")
 
 
 def run_reference(args):
@@ -175,7 +209,8 @@ def run_reference(args):
            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "config": {"workload": "c4 (sampled): fwd+bwd of one head, first 8192 of 188416 tokens, D=64",
                       "B": 1, "N": WORKLOAD["N"], "H": WORKLOAD["H"], "D": WORKLOAD["D"]},
-           "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")},
+           "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "kind", "sample", "cpu_model", "threads",
+                                              "extrapolated_full_c4_s", "extrapolated_note")},
            "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     del base
     print(json.dumps(out), flush=True)
@@ -228,10 +263,12 @@ def main():
     if args.deterministic:
         ctx.set_deterministic(True)
     dev = torch.device("cuda", local)
-    g = torch.Generator(device=dev).manual_seed(1234 + rank)
     shape = (B, Nl, H, D)
-    q, k, v, do = (torch.randn(shape, device=dev, generator=g, dtype=torch.float32).to(torch.bfloat16)
-                   for _ in range(4))
+    import synth
+    # counter-based draws of this rank's sequence shard of the global tensors: the data are
+    # identical for every P (synth/__init__.py); drawn on the host once, before any timing
+    host_in = synth.qkv(B, N, H, D, seed=synth.BASE_SEED, with_do=True, n0=rank * Nl, n1=(rank + 1) * Nl)
+    q, k, v, do = (t.to(dev) for t in host_in)
     fb, bb = (ua.lss_workspace_size if lss else ua.workspace_size)(B, N, H, D, P)
     ctx.workspace(max(fb, bb))
     out = torch.empty_like(q)
@@ -262,17 +299,22 @@ def main():
 
     # ---------------------------------------------------------------- timed
     ctx.enable_timing(True)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     barrier()
     torch.cuda.synchronize()
     with ClockSampler(enabled=(rank == 0)) as clk:
-        e0.record(stream)
-        for _ in range(args.steps):
+        evs[0].record(stream)
+        for i in range(args.steps):
             step()
-        e1.record(stream)
+            evs[i + 1].record(stream)
         torch.cuda.synchronize()
     barrier()
-    ms_total = max_over_ranks(e0.elapsed_time(e1))
+    ms_total = max_over_ranks(evs[0].elapsed_time(evs[-1]))
+    per_step = torch.tensor([evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)], dtype=torch.float64,
+                            device=dev)
+    if dist is not None:
+        dist.all_reduce(per_step, op=dist.ReduceOp.MAX)
+    per_step = per_step.cpu().tolist()
     ctx.enable_timing(False)
     phases = ctx.phase_times()
     calls1, bytes1 = ctx.comm_stats()
@@ -293,21 +335,18 @@ def main():
 
     kb = kstats("attn_bwd", bwd_f)
     kf = kstats("attn_fwd", fwd_f)
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tp):
-        try:
-            key = f"attn_bwd{'_det' if args.deterministic else ''}_D{D}_N{N}_P{P}"
-            traffic = None if lss or B != 1 else json.load(open(tp)).get(key)
-        except Exception:
-            traffic = None
+    ncu_b = None if lss or B != 1 else load_ncu("attn_bwd", D, N, P, args.deterministic)
+    ncu_f = None if lss or B != 1 else load_ncu("attn_fwd", D, N, P)
+    traffic = ncu_b.get("dram_bytes") if ncu_b else None
     roofline = {"bound": "tensor", "kernel": "attn_bwd_kernel", "achieved": kb["tflops"],
                 "peak": peaks["bf16_sustained"], "unit": UNIT, "frac": kb["tflops"] / peaks["bf16_sustained"],
                 "frac_of_burst": kb["tflops"] / peaks["bf16_burst"], "peak_source": peaks["source"] + " sustained",
-                "traffic": traffic,
+                "traffic": traffic, "traffic_source": ncu_b.get("source") if ncu_b else None,
                 "flops_per_launch": bwd_f / P, "flops_formula": "10*B*N^2*(H/P)*D per launch (5 GEMMs incl. recompute)"}
     fwd_roof = {"kernel": "attn_fwd_kernel", "achieved": kf["tflops"], "frac": kf["tflops"] / peaks["bf16_sustained"],
-                "avg_ms": kf["avg_ms"]}
+                "avg_ms": kf["avg_ms"], "traffic": ncu_f.get("dram_bytes") if ncu_f else None}
+    ncu = {"attn_bwd": ncu_b, "attn_fwd": ncu_f,
+           "note": "from the committed ncu --set full captures named in each entry's source (not this run)"}
     # our kernels per phase call: attn_bwd = bwd_prep + the backward kernel (+ the dQ kernel in
     # deterministic mode); the other non-a2a phases launch one kernel each (a2a phases: NCCL)
     per_call = {"attn_bwd": 3 if args.deterministic else 2}
@@ -324,7 +363,7 @@ def main():
         # double-buffered: step i+1's inputs upload and step i-1's results download while step i
         # computes (what a training loop's prefetcher does).  The timed region spans the first
         # upload to the last download.
-        hq, hk, hv, hd = (t.cpu().pin_memory() for t in (q, k, v, do))
+        hq, hk, hv, hd = (t.pin_memory() for t in host_in)
         hout = [[torch.empty(shape, dtype=torch.bfloat16).pin_memory() for _ in range(4)] for _ in range(2)]
         dins = [[torch.empty_like(q) for _ in range(4)] for _ in range(2)]
         douts = [[torch.empty_like(q) for _ in range(4)] for _ in range(2)]
@@ -397,7 +436,8 @@ def main():
                        "a2a": ("nccl all-gather/reduce-scatter" if lss else args.a2a) if P > 1 else "none",
                        "l2": "inputs larger than L2 (each q/k/v/dO shard "
                              f"{q.numel() * 2 / 1e6:.0f} MB; working set > 126 MB)",
-                       "inputs": "N(0,1) bf16, torch.randn seeded per rank",
+                       "inputs": "N(0,1) bf16 from synth/ (counter-based PCG64 blocks keyed by seed, tensor, b, h and "
+                                 "1024-token block: the global data are identical for every P), seed 1234",
                        "deterministic_bwd": bool(args.deterministic)},
             "tokens_per_s": B * N / (ms_step * 1e-3),
             "paper_context": PAPER_CONTEXT,
@@ -406,15 +446,23 @@ def main():
             "fwd_tflops_per_gpu_kernel": kf["tflops"], "bwd_tflops_per_gpu_kernel": kb["tflops"],
             "roofline": roofline, "roofline_fwd": fwd_roof,
             "phases_ms_per_step": phase_ms,
-            "a2a": {"calls": calls1 - calls0, "bytes_sent_per_rank": a2a_bytes,
-                    "GBps": (a2a_bytes / (a2a_ms * 1e-3) / 1e9) if a2a_ms > 0 else None},
+            "a2a": {"calls": calls1 - calls0, "bytes_sent_per_rank": a2a_bytes, "ms_per_step": a2a_ms / args.steps,
+                    "GBps": (a2a_bytes / (a2a_ms * 1e-3) / 1e9) if a2a_ms > 0 else None,
+                    "frac_of_nvlink": (a2a_bytes / (a2a_ms * 1e-3) / 1e9 / NVLINK_GBS) if a2a_ms > 0 else None,
+                    "nvlink_gbs": NVLINK_GBS,
+                    "note": "bytes this rank sent to other ranks / device time of the a2a phases (incl. NCCL launch"
+                            " and wait); per direction"},
+            "ncu": ncu,
+            "ms_per_step_median": statistics.median(per_step), "ms_per_step_min": min(per_step),
+            "ms_per_step_max": max(per_step),
             "gpu_launches": launches,
             "clocks": clk.summary(devices_in_use(P)),
             "e2e": e2e,
         }
         if P == 1 and not args.no_cpu_baseline:
             cb = cpu_baseline(steps=1)
-            res["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            res["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample", "cpu_model", "threads",
+                                                      "extrapolated_full_c4_s", "extrapolated_note")}
         print(json.dumps(res), flush=True)
     ctx.close()
     if dist is not None:

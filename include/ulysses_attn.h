@@ -24,9 +24,12 @@
  *  - scale = 1/sqrt(D); lse is the natural-log logsumexp of the scaled scores.
  *  - Calls are asynchronous and stream-ordered on `stream`.  For P > 1 they are
  *    COLLECTIVE: all P ranks call with identical (B, N, H, D, P) in the same
- *    order.  Argument validation happens on the host before anything is
- *    enqueued, so an invalid call returns the same status on every rank and
- *    never hangs a peer.
+ *    order.  Shape validation happens on the host before anything is
+ *    enqueued, so a shape error returns the same status on every rank and
+ *    never hangs a peer.  In UA_A2A_PEER mode a peer that never signals (a
+ *    rank that failed a per-rank check, died or diverged) is detected by a
+ *    bounded device-side wait (60 s) and reported as UA_ERR_CUDA by the next
+ *    call on that ctx; under UA_A2A_NCCL, NCCL's own error handling applies.
  *  - Errors: a non-UA_OK status; ua_last_error() returns a thread-local
  *    human-readable detail.  Asynchronous CUDA / NCCL faults surface as
  *    UA_ERR_CUDA / UA_ERR_NCCL on a later call.
@@ -254,7 +257,7 @@ ua_status ua_f32_to_bf16_bnhd(const float* src, void* dst, int64_t B, int64_t N,
  * The paper's other sequence-parallel strategy, Long Sequence Segmentation
  * (§1, §2.5: "sequences are divided into segments, with
  * each GPU computing a partial self-attention for its segment"; P:317, P:399:
- * it has no head limit, unlike Ulysses).  Reading (Q16): rank r keeps
+ * it has no head limit, unlike Ulysses).  Reading (R14): rank r keeps
  * its contiguous query segment of ALL H heads; K and V of every rank are
  * gathered (one fused all-gather, 1 collective call); each rank computes exact
  * attention of its N/P queries over all N keys.  Backward: dQ stays local; dK,
@@ -291,7 +294,7 @@ ua_status ua_lss_attn_bwd(ua_ctx* ctx, const void* q, const void* k, const void*
  *   w_o          : bf16 [E][E]
  *   dw_qkv, dw_o : fp32 [3E][E], [E][E]    (full gradients, identical on every rank)
  *   saved        : caller-owned, ua_layer_sizes' saved_bytes: q, k, v, o, lse of the forward
- * GEMMs: cuBLASLt, bf16 operands, fp32 accumulation (plain library GEMMs).
+ * GEMMs: this library's tcgen05 kernel (ua_gemm_bf16 below), bf16 operands, fp32 accumulation.
  * Collective calls per step: 2 forward, 3 backward (counted by ua_ctx_comm_stats).
  * Same validation (ua_validate) and conventions as the attention entry points. */
 ua_status ua_layer_sizes(int64_t B, int64_t N, int H, int D, int P, size_t* saved_bytes, size_t* fwd_bytes,
@@ -302,6 +305,18 @@ ua_status ua_layer_fwd(ua_ctx* ctx, const void* x, const void* w_qkv, const void
 ua_status ua_layer_bwd(ua_ctx* ctx, const void* x, const void* w_qkv, const void* w_o, const void* saved,
                        const void* dy, void* dx, float* dw_qkv, float* dw_o, int64_t B, int64_t N, int H, int D, int P,
                        void* workspace, size_t workspace_bytes, ua_stream_t stream);
+
+/* The projection GEMM itself (sm_100a tcgen05, TMA, TMEM):
+ *   C[M][N] = sum_{s < nseg} op(A[s]) op(B[s])   (fp32 accumulation; nseg 1..3
+ *   concatenates the reduction dimension over separate buffers)
+ *   a_mn = 0: A[s] bf16 [M][K] (op = identity);  a_mn = 1: A[s] bf16 [K][M] (op = transpose)
+ *   b_mn = 0: B[s] bf16 [N][K] (op = transpose); b_mn = 1: B[s] bf16 [K][N] (op = identity)
+ *   C: bf16 (c_f32 = 0) or fp32 [M][N].  Supported (a_mn, b_mn): (0,0) y = x W^T,
+ *   (0,1) dx = g W, (1,1) dW = g^T x; else UA_ERR_CUDA (invalid value).
+ * Pointers 16-B aligned; the leading dimensions (K, M or N) multiples of 8 elements.
+ * M, N, K < 2^31.  Stream-ordered, asynchronous, no ctx. */
+ua_status ua_gemm_bf16(int a_mn, int b_mn, int64_t M, int64_t N, int64_t K, const void* const* A, const void* const* B,
+                       int nseg, void* C, int c_f32, ua_stream_t stream);
 
 #ifdef __cplusplus
 }

@@ -9,7 +9,7 @@ GPU computing a partial self-attention for its segment".  BASELINE.json
 north_star: "online softmax and Long-Sequence-Segmentation chunking so the NxN
 matrix is never materialised".
 
-Reading (Q15): a key range [0, N) is split into contiguous segments
+Reading (R11): a key range [0, N) is split into contiguous segments
 s; each gives (O_s, lse_s) = exact attention of the queries over that segment
 only.  With lse = ln sum_s exp(lse_s) the full result is
     O = sum_s exp(lse_s - lse) O_s
@@ -49,7 +49,7 @@ def chunked_fwd(q, k, v, bounds):
 # --------------------------------------------------------------- LSS sequence parallelism
 # PAPER.md P:166 (§2.5): "sequences are divided into segments, with each GPU
 # computing a partial self-attention for its segment"; P:72 (§1): contiguous
-# segments, partial results aggregated.  Reading (Q16): rank r owns
+# segments, partial results aggregated.  Reading (R14): rank r owns
 # query/key/value rows [r*Nl, (r+1)*Nl) of every head; K and V are gathered,
 # so rank r's output rows are exact attention of its queries over all keys.
 # In the backward, rank r's queries contribute a PARTIAL sum to every dK_j,

@@ -34,7 +34,7 @@ EXPORTS = ("ua_version", "ua_status_string", "ua_last_error", "ua_validate", "ua
            "ua_f32_to_bf16_bnhd", "ua_lss_validate", "ua_lss_workspace_size", "ua_lss_attn_fwd", "ua_lss_attn_bwd",
            "ua_layer_sizes", "ua_layer_fwd", "ua_layer_bwd",
            "ua_pack_seq_to_head", "ua_unpack_head_to_seq", "ua_push_seq_to_head", "ua_head_attn_fwd",
-           "ua_head_attn_bwd_workspace_size", "ua_head_attn_bwd")
+           "ua_head_attn_bwd_workspace_size", "ua_head_attn_bwd", "ua_gemm_bf16")
 
 PHASES = ("pack_fwd", "a2a_fwd_in", "attn_fwd", "a2a_fwd_out", "unpack_fwd", "pack_bwd", "a2a_bwd_in",
           "attn_bwd", "dq_finalize", "a2a_bwd_out", "unpack_bwd")
@@ -99,6 +99,7 @@ def lib():
         L.ua_unpack_head_to_seq.argtypes = [pp, pp, i32, i64, i64, i32, i32, i32, vp]
         L.ua_push_seq_to_head.argtypes = [pp, i32, pp, i64, i64, i32, i32, i32, i32, vp, vp, vp]
         L.ua_head_attn_fwd.argtypes = [vp, vp, vp, vp, vp, i64, i64, i32, i32, i32, i32, pp, vp]
+        L.ua_gemm_bf16.argtypes = [i32, i32, i64, i64, i64, pp, pp, i32, vp, i32, vp]
         L.ua_head_attn_bwd_workspace_size.argtypes = [i64, i64, i32, i32, i32, ctypes.POINTER(sz)]
         L.ua_head_attn_bwd.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp, i64, i64, i32, i32, i32, i32, pp, i32, vp,
                                        sz, vp]
@@ -480,6 +481,19 @@ def head_attn_bwd(q, k, v, dout, lse, delta, P: int, rank: int, owners=None, det
                                   _ptr_array(owners) if owners is not None else None, 1 if deterministic else 0,
                                   _ptr(ws), ws.numel(), _stream(stream)))
     return None if owners is not None else grads
+
+
+def gemm(As, Bs, a_mn: bool, b_mn: bool, out_f32: bool = False, stream=None):
+    """C = sum_s op(A_s) op(B_s) on the library's tcgen05 GEMM (ua_gemm_bf16):
+    a_mn: A_s is [K][M] (transposed), else [M][K]; b_mn: B_s is [K][N], else
+    [N][K] (transposed).  Returns C [M][N] bf16 (or fp32)."""
+    A0, B0 = As[0], Bs[0]
+    M, K = (A0.shape[1], A0.shape[0]) if a_mn else (A0.shape[0], A0.shape[1])
+    N = B0.shape[1] if b_mn else B0.shape[0]
+    C = torch.empty((M, N), dtype=torch.float32 if out_f32 else torch.bfloat16, device=A0.device)
+    _check(lib().ua_gemm_bf16(int(a_mn), int(b_mn), M, N, K, _ptr_array(As), _ptr_array(Bs), len(As), _ptr(C),
+                              int(out_f32), _stream(stream)))
+    return C
 
 
 class UlyssesAttention(torch.autograd.Function):

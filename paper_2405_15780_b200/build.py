@@ -27,13 +27,6 @@ def _nccl_dirs():
     return inc, lib
 
 
-def _cublas_libdir():
-    """The cuBLASLt copy torch itself loads (site-packages nvidia/cublas), so one
-    libcublasLt.so.12 lives in the process; else the toolkit's."""
-    lib = os.path.join(sysconfig.get_paths()["purelib"], "nvidia", "cublas", "lib")
-    return lib if os.path.exists(os.path.join(lib, "libcublasLt.so.12")) else "/usr/local/cuda/lib64"
-
-
 def sources():
     return sorted(glob.glob(os.path.join(CSRC, "*.cpp")) + glob.glob(os.path.join(CSRC, "kernels", "*.cu")))
 
@@ -75,9 +68,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
             sys.stdout.write(out.decode())
         if p.returncode != 0:
             raise RuntimeError("nvcc failed:\n" + " ".join(cmd) + "\n" + out.decode())
-    lt = _cublas_libdir()
     link = [NVCC, *ARCH, "-shared", "-o", LIB + ".tmp", *objs, "-L", libdir, "-l:libnccl.so.2",
-            "-Xlinker", f"-rpath={libdir}", "-L", lt, "-l:libcublasLt.so.12", "-Xlinker", f"-rpath={lt}", "-lcudart"]
+            "-Xlinker", f"-rpath={libdir}", "-lcudart"]
     subprocess.check_call(link)
     os.replace(LIB + ".tmp", LIB)
     return LIB
@@ -103,10 +95,8 @@ def build_variant(name: str, defines: dict) -> str:
         o, _ = p.communicate()
         if p.returncode != 0:
             raise RuntimeError("nvcc failed:\n" + " ".join(cmd) + "\n" + o.decode())
-    lt = _cublas_libdir()
     subprocess.check_call([NVCC, *ARCH, "-shared", "-o", out, *objs, "-L", libdir, "-l:libnccl.so.2",
-                           "-Xlinker", f"-rpath={libdir}", "-L", lt, "-l:libcublasLt.so.12", "-Xlinker",
-                           f"-rpath={lt}", "-lcudart"])
+                           "-Xlinker", f"-rpath={libdir}", "-lcudart"])
     return out
 
 

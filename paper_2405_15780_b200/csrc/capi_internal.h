@@ -42,7 +42,6 @@ struct ua_ctx {
   // peer_err_host != 0 after a wait timed out; peer_err is its device alias.
   int* peer_err_host = nullptr;
   int* peer_err = nullptr;
-  void* lt = nullptr;  // cublasLtHandle_t of the projection layer (layer.cpp), created on first use
   int64_t step_fwd = 0, step_bwd = 0;
   cudaEvent_t get_event() {
     if (!pool.empty()) {
@@ -60,7 +59,7 @@ struct ua_ctx {
 namespace ua_internal {
 // Thread-local error detail + status (ua_last_error).
 ua_status fail(ua_status s, const char* fmt, ...);
-// Releases the projection layer's cuBLASLt handle (layer.cpp); called by ua_ctx_destroy.
+// Releases per-ctx state of the projection layer (layer.cpp; none at present); called by ua_ctx_destroy.
 void layer_release(ua_ctx* ctx);
 }  // namespace ua_internal
 

@@ -35,6 +35,9 @@
 //    elementwise warpgroups of 32 query columns (20 warps).
 //  * UA_BWD_EW_SPLIT (off): the same 32-column split with the dQ path (24 warps).
 //  * UA_BWD_KV_TMEM, UA_BWD_POLY_MOD, UA_BWD_STAGGER: see below.
+#include <cstdio>
+#include <cstdlib>
+
 #include "attn_common.cuh"
 #include "attn_kernels.h"
 #include "trace.cuh"
@@ -62,6 +65,9 @@
 #endif
 #ifndef UA_BWD_SEP_POLY_MOD
 #define UA_BWD_SEP_POLY_MOD 0   // same as UA_BWD_POLY_MOD for the separate-P^T variant (A/B: none is best)
+#endif
+#ifndef UA_BWD_PAIR
+#define UA_BWD_PAIR 1       // clusters of 2 CTAs on adjacent key tiles of a head sharing each Q / dO half tile (TMA multicast)
 #endif
 #ifndef UA_BWD_STAGGER
 #define UA_BWD_STAGGER 16   // query-tile window the persistent CTAs' start tiles are spread over
@@ -110,6 +116,12 @@ __host__ __device__ constexpr bool ws_sep_p() { return !kDq && BwdWsCfg<D>::kSep
 // 32 query columns (kSepP: 20 warps; with the dQ drain warpgroup: 24 warps).
 template <int D, bool kDq>
 __host__ __device__ constexpr bool ws_ew_split() { return kDq && UA_BWD_EW_SPLIT && D <= 64; }
+// Clusters of two CTAs that own key tiles 2m and 2m+1 of the same head and sweep
+// the same query tiles in the same order: every Q / dO half tile is read from L2
+// once per pair and multicast into both CTAs' ring slots (each CTA issues one of
+// the two loads), halving the per-SM Q / dO L2 read traffic.
+template <int D, bool kDq>
+__host__ __device__ constexpr bool ws_pair() { return kDq && UA_BWD_PAIR; }
 template <int D, bool kDq>
 __host__ __device__ constexpr int ws_threads() {
   return ws_sep_p<D, kDq>() ? 640 : (ws_ew_split<D, kDq>() ? 768 : 512);
@@ -127,6 +139,7 @@ __global__ void __launch_bounds__(ws_threads<D, kDq>(), 1) attn_bwd_ws_kernel(co
   constexpr int kEwCols = kSplit ? 32 : 64;       // query columns per elementwise thread and half tile
   constexpr int kEwEnd = kSplit ? 20 : 12;        // first warp after the elementwise warpgroups
   constexpr bool kBatch = kDq && !kSplit && UA_BWD_LDBATCH;   // 128 data registers per elementwise thread
+  constexpr bool kPair = ws_pair<D, kDq>();
   using G = TileGeom<D>;
   constexpr int kSl = C::kSlots;
   extern __shared__ uint8_t smem_raw[];
@@ -161,10 +174,18 @@ __global__ void __launch_bounds__(ws_threads<D, kDq>(), 1) attn_bwd_ws_kernel(co
   const int n_q = (p.n + 127) / 128;
   const int n_pad = n_q * 128;
   const int n_kt = (p.n_kv + 127) / 128;
-  const int n_items = p.batch * p.heads * n_kt;
+  // Work units: one key tile (kPair: a pair of adjacent key tiles, one per CTA of
+  // the cluster, both sweeping the same query tiles) of one (b, h), head-major.
+  const int crank = kPair ? int(cluster_ctarank()) : 0;
+  const int unit0 = kPair ? int(cluster_id_x()) : int(blockIdx.x);
+  const int n_units_grid = kPair ? int(num_clusters_x()) : int(gridDim.x);
+  const int n_kp = kPair ? (n_kt + 1) / 2 : n_kt;   // key tiles (pairs) per head; an odd tail pairs with an all-OOB tile
+  const int n_items = p.batch * p.heads * n_kp;
+  auto item_kt = [&](int u) { return kPair ? 2 * (u % n_kp) + crank : u % n_kp; };
+  auto item_bh = [&](int u) { return u / n_kp; };
   // Deterministic mode (no dQ reduction to spread out): every item sweeps from
   // tile 0, so the dK / dV summation order does not depend on the grid (P-invariant).
-  const int start = kDq ? int((int64_t(blockIdx.x) * C::kStagger) / gridDim.x) % n_q : 0;
+  const int start = kDq ? int((int64_t(unit0) * C::kStagger) / n_units_grid) % n_q : 0;
   auto qslot = [&](int s) { return sSlots + s * C::kSlotBytes; };
   auto doslot = [&](int s) { return sSlots + s * C::kSlotBytes + C::kHalfBytes; };
 
@@ -187,13 +208,14 @@ __global__ void __launch_bounds__(ws_threads<D, kDq>(), 1) attn_bwd_ws_kernel(co
     for (int i = 0; i < C::kNumDs; ++i) mbar_init(&ds_free[i], 1);
     for (int s = 0; s < kSl; ++s) {
       mbar_init(&slot_full[s], 1);
-      mbar_init(&slot_empty[s], 1);
+      mbar_init(&slot_empty[s], kPair ? 2 : 1);   // kPair: released by both CTAs' MMAs (the slot is refilled for both)
     }
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc<512>(tmem_slot);
   tc_fence_before();
   __syncthreads();
+  if constexpr (kPair) cluster_sync();   // the peer's barriers exist before any multicast load / commit
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
 
@@ -217,8 +239,8 @@ __global__ void __launch_bounds__(ws_threads<D, kDq>(), 1) attn_bwd_ws_kernel(co
       tma_prefetch_desc(&p.tm_v);
       tma_prefetch_desc(&p.tm_doh);
       int T = 0, it = 0;
-      for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
-        const int kt = item % n_kt, bh = item / n_kt;
+      for (int item = unit0; item < n_items; item += n_units_grid, ++it) {
+        const int kt = item_kt(item), bh = item_bh(item);
         const int b = bh / p.heads, h = bh % p.heads;
         if (it > 0) mbar_wait(kv_empty, (it - 1) & 1);
         mbar_arrive_expect_tx(kv_full, 2 * G::kTileBytes);
@@ -236,11 +258,17 @@ __global__ void __launch_bounds__(ws_threads<D, kDq>(), 1) attn_bwd_ws_kernel(co
             if (U >= kSl) mbar_wait(&slot_empty[s], ((U / kSl) & 1) ^ 1);
             UA_TEV(0, U, 2);
             mbar_arrive_expect_tx(&slot_full[s], C::kSlotBytes + C::kLsedBytes);
-            for (int a = 0; a < G::kAtoms; ++a) {
-              tma_load_4d(qslot(s) + a * 64 * G::kSw, &p.tm_qh, &slot_full[s], a * G::kAtomCols, tile * 128 + 64 * hh,
-                          h, b, kEvictLast);
-              tma_load_4d(doslot(s) + a * 64 * G::kSw, &p.tm_doh, &slot_full[s], a * G::kAtomCols,
-                          tile * 128 + 64 * hh, h, b, kEvictLast);
+            if constexpr (kPair) {  // Q_h (CTA 0) or dO_h (CTA 1), multicast into both CTAs' slot s
+              for (int a = 0; a < G::kAtoms; ++a)
+                tma_load_4d_mc((crank == 0 ? qslot(s) : doslot(s)) + a * 64 * G::kSw, crank == 0 ? &p.tm_qh : &p.tm_doh,
+                               &slot_full[s], a * G::kAtomCols, tile * 128 + 64 * hh, h, b, uint16_t(3), kEvictLast);
+            } else {
+              for (int a = 0; a < G::kAtoms; ++a) {
+                tma_load_4d(qslot(s) + a * 64 * G::kSw, &p.tm_qh, &slot_full[s], a * G::kAtomCols,
+                            tile * 128 + 64 * hh, h, b, kEvictLast);
+                tma_load_4d(doslot(s) + a * 64 * G::kSw, &p.tm_doh, &slot_full[s], a * G::kAtomCols,
+                            tile * 128 + 64 * hh, h, b, kEvictLast);
+              }
             }
             bulk_load(sLsed + s * 128, lsed_tile + 64 * hh, 256, &slot_full[s]);
             bulk_load(sLsed + s * 128 + 64, lsed_tile + 128 + 64 * hh, 256, &slot_full[s]);
@@ -305,7 +333,7 @@ __global__ void __launch_bounds__(ws_threads<D, kDq>(), 1) attn_bwd_ws_kernel(co
           mma_commit(&dp_full[hh]);
         };
         int T = 0, it = 0;
-        for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
+        for (int item = unit0; item < n_items; item += n_units_grid, ++it) {
           mbar_wait(C::kKvTmem ? kv_tmem : kv_full, it & 1);
           tc_fence_after();
           for (int hh = 0; hh < 2; ++hh) {
@@ -353,7 +381,7 @@ __global__ void __launch_bounds__(ws_threads<D, kDq>(), 1) attn_bwd_ws_kernel(co
         }
       } else {
       int T = 0, it = 0;
-      for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
+      for (int item = unit0; item < n_items; item += n_units_grid, ++it) {
         mbar_wait(C::kKvTmem ? kv_tmem : kv_full, it & 1);
         tc_fence_after();
         // first tile of the item
@@ -392,7 +420,10 @@ __global__ void __launch_bounds__(ws_threads<D, kDq>(), 1) attn_bwd_ws_kernel(co
               mma_ts(tbase + C::kColDK, tbase + C::kColDP + 64 * hh + kk * 8 + (kSplit && kk >= 2 ? 16 : 0),
                      mnmajor_desc_r<D, 64>(q_at(U), kk),
                      idesc_g, (acc || kk > 0) ? 1u : 0u);
-            mma_commit(&slot_empty[U % kSl]);
+            if constexpr (kPair)
+              mma_commit_mc(&slot_empty[U % kSl], uint16_t(3));   // free in both CTAs' view of the slot
+            else
+              mma_commit(&slot_empty[U % kSl]);
             UA_TEV(1, T, 3 + 4 * hh);
             auto issue_dq = [&]() {  // dQ(T) = dS K
               if (!C::kAliasDq && T > 0) {
@@ -448,8 +479,8 @@ __global__ void __launch_bounds__(ws_threads<D, kDq>(), 1) attn_bwd_ws_kernel(co
     const float c = p.scale_log2;
     const float2 c2 = make_float2(c, c);
     int T = 0, it = 0;
-    for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
-      const int kt = item % n_kt, bh = item / n_kt;
+    for (int item = unit0; item < n_items; item += n_units_grid, ++it) {
+      const int kt = item_kt(item), bh = item_bh(item);
       const int b = bh / p.heads, h = bh % p.heads;
       if constexpr (C::kKvTmem) {
         if (hh == 0 && g == 0) {  // copy this item's K, V rows (row j per thread) into TMEM as bf16 pairs
@@ -670,8 +701,8 @@ __global__ void __launch_bounds__(ws_threads<D, kDq>(), 1) attn_bwd_ws_kernel(co
     constexpr int kCols = D == 128 ? 64 : (D == 80 ? 96 : D);
     constexpr int kRounds = D == 128 ? 2 : 1;
     int T = 0;
-    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-      const int bh = item / n_kt;
+    for (int item = unit0; item < n_items; item += n_units_grid) {
+      const int bh = item_bh(item);
       for (int t = 0; t < n_q; ++t, ++T) {
         const int tile = (start + t) % n_q;
         if (r == 0) UA_TEV(4, T, 1);
@@ -731,6 +762,7 @@ __global__ void __launch_bounds__(ws_threads<D, kDq>(), 1) attn_bwd_ws_kernel(co
 
   tc_fence_before();
   __syncthreads();
+  if constexpr (kPair) cluster_sync();   // no multicast load / commit may target a CTA that has exited
   if (warp == 1) tmem_free<512>(tbase);
 }
 
@@ -741,12 +773,40 @@ cudaError_t launch_bwd_ws_impl(const BwdParams& p, cudaStream_t stream) {
   if (num_sms <= 0) return cudaErrorNoDevice;
   cudaError_t e = set_max_smem(attn_bwd_ws_kernel<D, kDq>, C::kSmemBytes);
   if (e != cudaSuccess) return e;
-  const int64_t items = int64_t(p.batch) * p.heads * ((p.n_kv + 127) / 128);
-  const int grid = int(items < num_sms ? items : num_sms);
+  const int n_kt = (p.n_kv + 127) / 128;
+  constexpr bool kPair = ws_pair<D, kDq>();
+  const int64_t units = int64_t(p.batch) * p.heads * (kPair ? (n_kt + 1) / 2 : n_kt);
 #if UA_TRACE
   trace_reset();
 #endif
-  attn_bwd_ws_kernel<D, kDq><<<grid, ws_threads<D, kDq>(), C::kSmemBytes, stream>>>(p);
+  if constexpr (kPair) {
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.blockDim = dim3(ws_threads<D, kDq>());
+    cfg.dynamicSmemBytes = C::kSmemBytes;
+    cfg.stream = stream;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int max_clusters = 0;   // co-resident pairs (an SM left alone in its GPC cannot host half of one)
+    cfg.gridDim = dim3(2 * (num_sms / 2));
+    e = cudaOccupancyMaxActiveClusters(&max_clusters, attn_bwd_ws_kernel<D, kDq>, &cfg);
+    if (std::getenv("UA_VERBOSE"))
+      std::fprintf(stderr, "[ua] attn_bwd_ws<%d>: %d SMs, max active clusters of 2: %d (%s)\n", D, num_sms,
+                   max_clusters, cudaGetErrorString(e));
+    if (e != cudaSuccess || max_clusters < 1) max_clusters = num_sms / 2;
+    cudaGetLastError();
+    const int64_t pairs = units < max_clusters ? units : max_clusters;
+    cfg.gridDim = dim3(unsigned(2 * pairs));
+    e = cudaLaunchKernelEx(&cfg, attn_bwd_ws_kernel<D, kDq>, p);
+    if (e != cudaSuccess) return e;
+  } else {
+    const int grid = int(units < num_sms ? units : num_sms);
+    attn_bwd_ws_kernel<D, kDq><<<grid, ws_threads<D, kDq>(), C::kSmemBytes, stream>>>(p);
+  }
 #if UA_TRACE
   trace_dump("bwd");
 #endif

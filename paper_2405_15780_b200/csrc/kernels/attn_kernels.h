@@ -94,6 +94,26 @@ inline int current_num_sms() {
 }
 
 cudaError_t launch_attn_fwd(const FwdParams& p, int D, int B, int heads, cudaStream_t stream);
+
+// ---- projection GEMMs of the attention layer (gemm.cu) ---------------------------
+// C[M][N] = sum_{s < nseg} op(A_s) op(B_s), bf16 operands, fp32 accumulation.
+// tm_a[s]: a_mn ? A stored [K][M] (2-D map {M, K}, box {64, 64})
+//               : A stored [M][K] (map {K, M}, box {64, 128});
+// tm_b[s]: b_mn ? B stored [K][N] (map {N, K}, box {64, 64})
+//               : B stored [N][K] (map {K, N}, box {64, gemm_bn(N)}); all SWIZZLE_128B.
+constexpr int kGemmMaxSeg = 3;
+struct alignas(64) GemmParams {
+  CUtensorMap tm_a[kGemmMaxSeg];
+  CUtensorMap tm_b[kGemmMaxSeg];
+  void* c;          // row-major [M][ldc], bf16 (c_f32 == 0) or fp32
+  int64_t ldc;
+  int c_f32;
+  int M, N, K;      // K per segment
+  int nseg;
+  bool a_mn, b_mn;
+};
+int gemm_bn(int N);   // CTA tile width used for N (the K-major B map's box rows)
+cudaError_t launch_gemm(const GemmParams& p, cudaStream_t stream);
 // D <= 64 column-split forward (attn_fwd_split.cu); launch_attn_fwd dispatches to it when enabled.
 cudaError_t launch_attn_fwd_split(const FwdParams& p, int D, int B, int heads, cudaStream_t stream);
 // The backward (attn_bwd_ws.cu): persistent KV-stationary kernel (+ the query-stationary dQ kernel

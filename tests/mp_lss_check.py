@@ -3,7 +3,7 @@ tests/test_multigpu.py as
     torchrun --nproc-per-node P tests/mp_lss_check.py --N .. --H .. --D .. [--B ..]
 Each rank feeds its contiguous sequence segment (sliced from the same synth
 global tensors) through ua_lss_attn_fwd / _bwd with P ranks (PAPER.md P:72,
-P:166; Q16); rank 0 gathers and checks:
+P:166; R14); rank 0 gathers and checks:
   * P-way forward == P=1 forward, bitwise (each query row sees the same key
     tiles in the same order);
   * out / lse / dq / dk / dv against the fp64 dense oracle (tests/parity.py);
@@ -87,8 +87,10 @@ def main():
         assert np.array_equal(out_g, r1.out.float().cpu().numpy()), "P-way LSS forward != P=1 forward"
         assert np.array_equal(lse_g, r1.lse.cpu().numpy()), "P-way LSS lse != P=1 lse"
         for x, y in zip((dq_g, dk_g, dv_g), g1):
-            # dK, dV: fp32 partial sums vs one TMEM accumulation, each rounded to bf16
-            # once -> they may differ by an ulp (2^-7 relative) on large sigma=2 gradients
+            # dK, dV: P fp32 partial sums (reduce-scattered) vs one TMEM accumulation, each
+            # rounded to bf16 once -> they may differ by one bf16 ulp (2^-7 relative) plus the
+            # fp32 reassociation of the partials (R18); the oracle gates below are
+            # the parity bar, this cross-check only bounds the P-way vs P = 1 difference
             y = y.float().cpu().numpy()
             assert (np.abs(x - y) - (2e-2 + 2.0 ** -7 * np.abs(y))).max() <= 0
         f64 = [synth.to_f64(t) for t in (q, k, v, do)]
