@@ -86,17 +86,37 @@ static double attend_row(const double* qi, const double* kb, const double* vb,
                          int64_t Nk, int64_t rs, int64_t D, double scale,
                          double* s, double* o, double* oabs) {
   double m = -INFINITY;
-  for (int64_t j = 0; j < Nk; ++j) {
-    s[j] = scale * dot(qi, kb + j * rs, D);
-    if (s[j] > m) m = s[j];
+  int64_t j = 0;
+  /* Four keys at a time: four independent dot products, each summed over d in
+   * the same order as dot() (bitwise-identical scores; only the instruction
+   * schedule differs, so the loop is not bound by one add-latency chain). */
+  for (; j + 4 <= Nk; j += 4) {
+    const double* k0 = kb + j * rs;
+    const double* k1 = k0 + rs;
+    const double* k2 = k1 + rs;
+    const double* k3 = k2 + rs;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    for (int64_t d = 0; d < D; ++d) {
+      a0 += qi[d] * k0[d];
+      a1 += qi[d] * k1[d];
+      a2 += qi[d] * k2[d];
+      a3 += qi[d] * k3[d];
+    }
+    s[j] = scale * a0;
+    s[j + 1] = scale * a1;
+    s[j + 2] = scale * a2;
+    s[j + 3] = scale * a3;
   }
+  for (; j < Nk; ++j) s[j] = scale * dot(qi, kb + j * rs, D);
+  for (j = 0; j < Nk; ++j)
+    if (s[j] > m) m = s[j];
   double l = 0.0;
-  for (int64_t j = 0; j < Nk; ++j) l += exp(s[j] - m);
+  for (j = 0; j < Nk; ++j) l += exp(s[j] - m);
   double lse = m + log(l);
   for (int64_t d = 0; d < D; ++d) o[d] = 0.0;
   if (oabs)
     for (int64_t d = 0; d < D; ++d) oabs[d] = 0.0;
-  for (int64_t j = 0; j < Nk; ++j) {
+  for (j = 0; j < Nk; ++j) {
     double p = exp(s[j] - lse);
     const double* vj = vb + j * rs;
     for (int64_t d = 0; d < D; ++d) o[d] += p * vj[d];
