@@ -353,6 +353,10 @@ def main():
     launches = sum(n * per_call.get(name, 1) for name, (ms, n) in phases.items() if not name.startswith("a2a"))
     phase_ms = {name: ms / args.steps for name, (ms, n) in phases.items() if n}
     a2a_ms = sum(ms for name, (ms, n) in phases.items() if name.startswith("a2a"))
+    comm_ms = sum(ms for name, (ms, n) in phases.items() if name.startswith(("a2a", "pack", "unpack")))
+    # peer transport: the NVLink stores happen in the pack / attention / finaliser kernels, so the
+    # transfer time is the data-movement phases, not the (flag-wait only) a2a phases
+    xfer_ms = comm_ms if (P > 1 and not lss and args.a2a == "peer") else a2a_ms
     a2a_bytes = bytes1 - bytes0
 
     # ---------------------------------------------------------------- e2e
@@ -447,11 +451,16 @@ def main():
             "roofline": roofline, "roofline_fwd": fwd_roof,
             "phases_ms_per_step": phase_ms,
             "a2a": {"calls": calls1 - calls0, "bytes_sent_per_rank": a2a_bytes, "ms_per_step": a2a_ms / args.steps,
-                    "GBps": (a2a_bytes / (a2a_ms * 1e-3) / 1e9) if a2a_ms > 0 else None,
-                    "frac_of_nvlink": (a2a_bytes / (a2a_ms * 1e-3) / 1e9 / NVLINK_GBS) if a2a_ms > 0 else None,
+                    "comm_ms_per_step": comm_ms / args.steps,
+                    "comm_share_of_step": (comm_ms / args.steps) / ms_step if P > 1 else 0.0,
+                    "GBps": (a2a_bytes / (xfer_ms * 1e-3) / 1e9) if xfer_ms > 0 else None,
+                    "frac_of_nvlink": (a2a_bytes / (xfer_ms * 1e-3) / 1e9 / NVLINK_GBS) if xfer_ms > 0 else None,
                     "nvlink_gbs": NVLINK_GBS,
-                    "note": "bytes this rank sent to other ranks / device time of the a2a phases (incl. NCCL launch"
-                            " and wait); per direction"},
+                    "note": ("bytes this rank sent to other ranks / device time of the phases that move them: "
+                             + ("the a2a phases (NCCL send/recv incl. launch and wait)" if args.a2a == "nccl" or lss
+                                else "pack_push + flag waits + copy-out (the peer stores happen inside the pack and "
+                                     "attention kernels)")
+                             + "; per direction.  comm_ms = pack + a2a + unpack phases per step")},
             "ncu": ncu,
             "ms_per_step_median": statistics.median(per_step), "ms_per_step_min": min(per_step),
             "ms_per_step_max": max(per_step),

@@ -91,9 +91,10 @@ def main():
             sel = bh[:, 1] == hi
             gate_lse(lse_np[0, h - rank * hl, gi], l_ref[sel])
 
-    # ---- dK / dV at sampled KEY rows of head 0, element by element (c3, c4: the oracle
-    # recomputes that head's lse / Delta in a few minutes; c5 is out of its reach)
-    if N <= 200000:
+    # ---- dK / dV at sampled KEY rows of head 0, element by element (c3, c4 at P > 1: the
+    # oracle recomputes that head's lse / Delta in a few minutes; c5 is out of its reach; P = 1
+    # is covered by tests/test_bwd_gpu.py::test_bwd_full_size_sampled_rows)
+    if N <= 200000 and P > 1:
         keys_local = np.array(rows)
         local = dict(keys=(keys_local + rank * Nl).tolist(),
                      dk=dk[0, torch.from_numpy(keys_local).to(dev), 0].float().cpu().numpy(),
