@@ -278,6 +278,27 @@ ua_status ua_lss_attn_bwd(ua_ctx* ctx, const void* q, const void* k, const void*
                           const void* dout, void* dq, void* dk, void* dv, int64_t B, int64_t N, int H, int D, int P,
                           void* workspace, size_t workspace_bytes, ua_stream_t stream);
 
+/* LSS rank-local steps (no communication; the LSS analogue of the Ulysses
+ * rank-local steps above, R14): what rank r computes between the collectives.
+ *   q, out, dout, dq : bf16 [B][N/P][H][D]   this rank's query segment
+ *   k_full, v_full   : bf16 [N][B][H][D]     every rank's keys / values in rank
+ *                      order (the all-gather's output: rank p's tokens at rows
+ *                      [p N/P, (p+1) N/P); for B == 1 each rank's [1][N/P][H][D]
+ *                      shard is that block as is)
+ *   lse              : fp32 [B][H][N/P]
+ *   dk_part, dv_part : fp32 [N][B][H][D]     partial sums over THIS rank's
+ *                      queries for all N keys (written; their sum over ranks,
+ *                      scattered to the key owners, is dK, dV: the reduce-scatter)
+ *   workspace        : >= ua_lss_rank_bwd_workspace_size bytes.
+ * Constraints and errors as ua_lss_validate plus pointer checks. */
+ua_status ua_lss_rank_fwd(const void* q, const void* k_full, const void* v_full, void* out, float* lse, int64_t B,
+                          int64_t N, int H, int D, int P, ua_stream_t stream);
+ua_status ua_lss_rank_bwd_workspace_size(int64_t B, int64_t N, int H, int D, int P, size_t* bytes);
+ua_status ua_lss_rank_bwd(const void* q, const void* k_full, const void* v_full, const void* out, const float* lse,
+                          const void* dout, void* dq, float* dk_part, float* dv_part, int64_t B, int64_t N, int H,
+                          int D, int P, int deterministic, void* workspace, size_t workspace_bytes,
+                          ua_stream_t stream);
+
 /* ------------------------------------------------------------- attention layer
  * The rest of the paper's attention layer around the Ulysses attention
  * (SURVEY §8(f)-3): the Q/K/V and output projections and the SP group's

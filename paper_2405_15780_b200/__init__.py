@@ -34,7 +34,8 @@ EXPORTS = ("ua_version", "ua_status_string", "ua_last_error", "ua_validate", "ua
            "ua_f32_to_bf16_bnhd", "ua_lss_validate", "ua_lss_workspace_size", "ua_lss_attn_fwd", "ua_lss_attn_bwd",
            "ua_layer_sizes", "ua_layer_fwd", "ua_layer_bwd",
            "ua_pack_seq_to_head", "ua_unpack_head_to_seq", "ua_push_seq_to_head", "ua_head_attn_fwd",
-           "ua_head_attn_bwd_workspace_size", "ua_head_attn_bwd", "ua_gemm_bf16")
+           "ua_head_attn_bwd_workspace_size", "ua_head_attn_bwd", "ua_gemm_bf16",
+           "ua_lss_rank_fwd", "ua_lss_rank_bwd_workspace_size", "ua_lss_rank_bwd")
 
 PHASES = ("pack_fwd", "a2a_fwd_in", "attn_fwd", "a2a_fwd_out", "unpack_fwd", "pack_bwd", "a2a_bwd_in",
           "attn_bwd", "dq_finalize", "a2a_bwd_out", "unpack_bwd")
@@ -100,6 +101,9 @@ def lib():
         L.ua_push_seq_to_head.argtypes = [pp, i32, pp, i64, i64, i32, i32, i32, i32, vp, vp, vp]
         L.ua_head_attn_fwd.argtypes = [vp, vp, vp, vp, vp, i64, i64, i32, i32, i32, i32, pp, vp]
         L.ua_gemm_bf16.argtypes = [i32, i32, i64, i64, i64, pp, pp, i32, vp, i32, vp]
+        L.ua_lss_rank_fwd.argtypes = [vp, vp, vp, vp, vp, i64, i64, i32, i32, i32, vp]
+        L.ua_lss_rank_bwd_workspace_size.argtypes = [i64, i64, i32, i32, i32, ctypes.POINTER(sz)]
+        L.ua_lss_rank_bwd.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp, i64, i64, i32, i32, i32, i32, vp, sz, vp]
         L.ua_head_attn_bwd_workspace_size.argtypes = [i64, i64, i32, i32, i32, ctypes.POINTER(sz)]
         L.ua_head_attn_bwd.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp, i64, i64, i32, i32, i32, i32, pp, i32, vp,
                                        sz, vp]
@@ -481,6 +485,35 @@ def head_attn_bwd(q, k, v, dout, lse, delta, P: int, rank: int, owners=None, det
                                   _ptr_array(owners) if owners is not None else None, 1 if deterministic else 0,
                                   _ptr(ws), ws.numel(), _stream(stream)))
     return None if owners is not None else grads
+
+
+def lss_rank_fwd(q, k_full, v_full, P: int, out=None, lse=None, stream=None):
+    """LSS compute of one rank (no communication): q bf16 [B][N/P][H][D] (its
+    query segment), k_full, v_full bf16 [N][B][H][D] (all ranks' keys, rank
+    order).  Returns (out [B][N/P][H][D] bf16, lse [B][H][N/P] fp32)."""
+    B, Nl, H, D = q.shape
+    out = torch.empty_like(q) if out is None else out
+    lse = torch.empty((B, H, Nl), dtype=torch.float32, device=q.device) if lse is None else lse
+    _check(lib().ua_lss_rank_fwd(_ptr(q), _ptr(k_full), _ptr(v_full), _ptr(out), _ptr(lse), B, Nl * P, H, D, P,
+                                 _stream(stream)))
+    return out, lse
+
+
+def lss_rank_bwd(q, k_full, v_full, out, lse, dout, P: int, deterministic=False, stream=None):
+    """LSS backward compute of one rank: returns (dq bf16 [B][N/P][H][D],
+    dk_part, dv_part fp32 [N][B][H][D] = partial sums over this rank's queries)."""
+    B, Nl, H, D = q.shape
+    N = Nl * P
+    n = ctypes.c_size_t(0)
+    _check(lib().ua_lss_rank_bwd_workspace_size(B, N, H, D, P, ctypes.byref(n)))
+    ws = torch.empty(max(n.value, 256), dtype=torch.uint8, device=q.device)
+    dq = torch.empty_like(q)
+    dk_part = torch.empty((N, B, H, D), dtype=torch.float32, device=q.device)
+    dv_part = torch.empty_like(dk_part)
+    _check(lib().ua_lss_rank_bwd(_ptr(q), _ptr(k_full), _ptr(v_full), _ptr(out), _ptr(lse), _ptr(dout), _ptr(dq),
+                                 _ptr(dk_part), _ptr(dv_part), B, N, H, D, P, 1 if deterministic else 0, _ptr(ws),
+                                 ws.numel(), _stream(stream)))
+    return dq, dk_part, dv_part
 
 
 def gemm(As, Bs, a_mn: bool, b_mn: bool, out_f32: bool = False, stream=None):

@@ -154,8 +154,22 @@ BwdPlan plan_bwd(const Shape& s) {
 }
 
 // LSS plans (P > 1).  KV gathered layout [N][B][H][D] (rank p's tokens at rows p*Nl..).
+// Rank-local LSS backward workspace: Delta [Nl][B][H] fp32, dq_acc [B*H][Nl_pad][D] fp32,
+// (lse, Delta) table [B*H][Nl_pad] float2.
+struct LssRankPlan {
+  size_t delta = 0, dq_acc = 0, lsed = 0, total = 0;
+};
+LssRankPlan plan_lss_rank(const Shape& s) {
+  LssRankPlan p;
+  const int64_t n_pad = (s.Nl + 127) / 128 * 128;
+  p.delta = 0;
+  p.dq_acc = align_up(p.delta + size_t(s.B * s.Nl * s.H) * 4);
+  p.lsed = align_up(p.dq_acc + size_t(s.B * s.H * n_pad * s.D) * 4);
+  p.total = align_up(p.lsed + size_t(s.B * s.H * n_pad) * 8);
+  return p;
+}
 struct LssPlan {
-  size_t kv_send = 0, kv_full = 0, delta = 0, dq_acc = 0, lsed = 0, part = 0, red = 0, total = 0;
+  size_t kv_send = 0, kv_full = 0, rank = 0, part = 0, red = 0, total = 0;
 };
 LssPlan plan_lss(const Shape& s, bool bwd) {
   LssPlan p;
@@ -165,11 +179,8 @@ LssPlan plan_lss(const Shape& s, bool bwd) {
   p.kv_full = align_up(p.kv_send + 2 * S);          // [2][N][B][H][D] bf16
   p.total = align_up(p.kv_full + 2 * S * s.P);
   if (!bwd) return p;
-  const int64_t n_pad = (s.Nl + 127) / 128 * 128;
-  p.delta = p.total;                                // [Nl][B][H] fp32
-  p.dq_acc = align_up(p.delta + size_t(s.B * s.Nl * s.H) * 4);         // [B*H][Nl_pad][D] fp32
-  p.lsed = align_up(p.dq_acc + size_t(s.B * s.H * n_pad * s.D) * 4);   // [B*H][Nl_pad] float2
-  p.part = align_up(p.lsed + size_t(s.B * s.H * n_pad) * 8);           // [2][N][B][H][D] fp32 partial dK, dV
+  p.rank = p.total;                                 // rank-local backward workspace (LssRankPlan)
+  p.part = align_up(p.rank + plan_lss_rank(s).total);                   // [2][N][B][H][D] fp32 partial dK, dV
   p.red = align_up(p.part + 2 * S * 2 * s.P);                          // [2][Nl][B][H][D] fp32 reduced
   p.total = align_up(p.red + 2 * S * 2);
   return p;
@@ -989,6 +1000,50 @@ ua_status lss_gather_kv(ua_ctx* ctx, const Shape& s, const void* k, const void* 
   return UA_OK;
 }
 
+// LSS compute of one rank (no communication): its N/P queries of every head over all N keys.
+//   q, dout, out [B][Nl][H][D] bf16 (sequence shard); kf, vf [N][B][H][D] bf16 (the gathered keys);
+//   lse [B][H][Nl]; dk_part, dv_part fp32 [N][B][H][D] (partial sums over this rank's queries).
+ua_status lss_rank_fwd(ua_ctx* ctx, const Shape& s, const void* q, const void* kf, const void* vf, void* out,
+                       float* lse, cudaStream_t stream) {
+  const int64_t H = s.H, D = s.D;
+  const int64_t qsn = H * D, qsh = D, qsb = s.Nl * H * D;
+  const Rows qr{q, qsn, qsh, qsb, s.Nl};
+  const Rows kvr{nullptr, s.B * H * D, D, H * D, s.N};
+  ua::ViewArg o{out, qsn, qsh, qsb};
+  Phase ph(ctx, UA_PHASE_ATTN_FWD, stream);
+  return launch_attention_fwd(qr, kf, vf, kvr, o, nullptr, 0, 0, 0, lse, s.Nl, H * s.Nl, s.B, s.H, s.D, 0, s.N, stream);
+}
+
+ua_status lss_rank_bwd(ua_ctx* ctx, const Shape& s, const void* q, const void* kf, const void* vf, const void* out,
+                       const float* lse, const void* dout, void* dq, float* dk_part, float* dv_part, int deterministic,
+                       char* ws, cudaStream_t stream) {
+  const int64_t H = s.H, D = s.D, Nl = s.Nl;
+  const LssRankPlan plan = plan_lss_rank(s);
+  const int64_t n_pad = (Nl + 127) / 128 * 128;
+  const float scale = float(1.0 / std::sqrt(double(D)));
+  float* delta = reinterpret_cast<float*>(ws + plan.delta);
+  float* dq_acc = reinterpret_cast<float*>(ws + plan.dq_acc);
+  {  // Delta[t][b][h] = sum_d dO.O (fp32), local queries
+    Phase ph(ctx, UA_PHASE_PACK_BWD, stream);
+    UA_CUDA(ua::launch_pack(nullptr, nullptr, 0, s.B, Nl, s.H, s.D, 1, dout, out, delta, stream));
+  }
+  const int64_t qsn = H * D, qsh = D, qsb = Nl * H * D;
+  const int64_t ksn = s.B * H * D, ksh = D, ksb = H * D;
+  {  // local dQ; dK, dV partial sums over the local queries for all N keys (fp32)
+    Phase ph(ctx, UA_PHASE_ATTN_BWD, stream);
+    UA_CUDA(cudaMemsetAsync(dq_acc, 0, size_t(s.B * H * n_pad * D) * 4, stream));
+    const Rows qr{q, qsn, qsh, qsb, Nl};
+    const Rows kvr{nullptr, ksn, ksh, ksb, s.N};
+    ua::ViewArg vdk{dk_part, ksn, ksh, ksb}, vdv{dv_part, ksn, ksh, ksb};
+    UA_TRY(launch_attention_bwd(qr, dout, kf, vf, kvr, vdk, vdv, 1, dq_acc, lse, Nl, H * Nl, delta, s.B * H, 1, s.H,
+                                s.B, s.H, s.D, reinterpret_cast<float2*>(ws + plan.lsed), deterministic, stream));
+  }
+  Phase ph(ctx, UA_PHASE_DQ_FINALIZE, stream);
+  ua::ViewArg vdq{dq, qsn, qsh, qsb};
+  UA_CUDA(ua::launch_dq_finalize(dq_acc, vdq, s.B, Nl, s.H, s.D, scale, stream));
+  return UA_OK;
+}
+
 ua_status lss_check_call(ua_ctx* ctx, int64_t B, int64_t N, int H, int D, int P, std::initializer_list<const void*> ptrs,
                          size_t need, void* workspace, size_t workspace_bytes) {
   UA_TRY(ua_lss_validate(B, N, H, D, P));
@@ -1016,13 +1071,7 @@ ua_status ua_lss_attn_fwd(ua_ctx* ctx, const void* q, const void* k, const void*
   UA_TRY(lss_gather_kv(ctx, s, k, v, ws, plan, UA_PHASE_PACK_FWD, UA_PHASE_A2A_FWD_IN, stream));
   // exact attention of the local query segment over all N keys, every head
   const size_t S = size_t(s.shard()) * 2;
-  const int64_t qsn = int64_t(H) * D, qsh = D, qsb = s.Nl * H * D;
-  const Rows qr{q, qsn, qsh, qsb, s.Nl};
-  const Rows kvr{nullptr, B * int64_t(H) * D, D, int64_t(H) * D, N};
-  ua::ViewArg o{out, qsn, qsh, qsb};
-  Phase ph(ctx, UA_PHASE_ATTN_FWD, stream);
-  return launch_attention_fwd(qr, ws + plan.kv_full, ws + plan.kv_full + S * P, kvr, o, nullptr, 0, 0, 0, lse, s.Nl,
-                              int64_t(H) * s.Nl, B, H, D, 0, N, stream);
+  return lss_rank_fwd(ctx, s, q, ws + plan.kv_full, ws + plan.kv_full + S * P, out, lse, stream);
 }
 
 ua_status ua_lss_attn_bwd(ua_ctx* ctx, const void* q, const void* k, const void* v, const void* out, const float* lse,
@@ -1039,35 +1088,12 @@ ua_status ua_lss_attn_bwd(ua_ctx* ctx, const void* q, const void* k, const void*
   char* ws = static_cast<char*>(workspace);
   const size_t S = size_t(s.shard()) * 2;
   const int64_t Nl = s.Nl;
-  const int64_t n_pad = (Nl + 127) / 128 * 128;
-  const float scale = float(1.0 / std::sqrt(double(D)));
   UA_TRY(lss_gather_kv(ctx, s, k, v, ws, plan, UA_PHASE_PACK_BWD, UA_PHASE_A2A_BWD_IN, stream));
-  float* delta = reinterpret_cast<float*>(ws + plan.delta);
-  float* dq_acc = reinterpret_cast<float*>(ws + plan.dq_acc);
   float* part = reinterpret_cast<float*>(ws + plan.part);
   float* red = reinterpret_cast<float*>(ws + plan.red);
-  {  // Delta[t][b][h] = sum_d dO.O (fp32), local queries
-    Phase ph(ctx, UA_PHASE_PACK_BWD, stream);
-    UA_CUDA(ua::launch_pack(nullptr, nullptr, 0, B, Nl, H, D, 1, dout, out, delta, stream));
-  }
-  const int64_t qsn = int64_t(H) * D, qsh = D, qsb = Nl * H * D;
-  const int64_t ksn = B * int64_t(H) * D, ksh = D, ksb = int64_t(H) * D;
   const size_t PE = size_t(s.shard()) * s.P;  // elements of one [N][B][H][D] tensor
-  {  // local dQ; dK, dV partial sums over the local queries for all N keys (fp32)
-    Phase ph(ctx, UA_PHASE_ATTN_BWD, stream);
-    UA_CUDA(cudaMemsetAsync(dq_acc, 0, size_t(B * H * n_pad * D) * 4, stream));
-    const Rows qr{q, qsn, qsh, qsb, Nl};
-    const Rows kvr{nullptr, ksn, ksh, ksb, N};
-    ua::ViewArg vdk{part, ksn, ksh, ksb}, vdv{part + PE, ksn, ksh, ksb};
-    UA_TRY(launch_attention_bwd(qr, dout, ws + plan.kv_full, ws + plan.kv_full + S * P, kvr, vdk, vdv, 1, dq_acc, lse,
-                                Nl, int64_t(H) * Nl, delta, B * int64_t(H), 1, H, B, H, D,
-                                reinterpret_cast<float2*>(ws + plan.lsed), ctx->deterministic, stream));
-  }
-  {
-    Phase ph(ctx, UA_PHASE_DQ_FINALIZE, stream);
-    ua::ViewArg vdq{dq, qsn, qsh, qsb};
-    UA_CUDA(ua::launch_dq_finalize(dq_acc, vdq, B, Nl, H, D, scale, stream));
-  }
+  UA_TRY(lss_rank_bwd(ctx, s, q, ws + plan.kv_full, ws + plan.kv_full + S * P, out, lse, dout, dq, part, part + PE,
+                      ctx->deterministic, ws + plan.rank, stream));
   {  // dK, dV partials summed over ranks into the key owners (one fused reduce-scatter)
     Phase ph(ctx, UA_PHASE_A2A_BWD_OUT, stream);
     UA_NCCL(ncclGroupStart());
@@ -1092,6 +1118,39 @@ ua_status ua_lss_attn_bwd(ua_ctx* ctx, const void* q, const void* k, const void*
     }
   }
   return UA_OK;
+}
+
+ua_status ua_lss_rank_fwd(const void* q, const void* k_full, const void* v_full, void* out, float* lse, int64_t B,
+                          int64_t N, int H, int D, int P, ua_stream_t stream) {
+  UA_TRY(ua_lss_validate(B, N, H, D, P));
+  UA_TRY(check_ptrs({q, k_full, v_full, out, lse}));
+  UA_TRY(check_device());
+  UA_TRY(check_async(nullptr));
+  return lss_rank_fwd(nullptr, make_shape(B, N, H, D, P), q, k_full, v_full, out, lse,
+                      reinterpret_cast<cudaStream_t>(stream));
+}
+
+ua_status ua_lss_rank_bwd_workspace_size(int64_t B, int64_t N, int H, int D, int P, size_t* bytes) {
+  UA_TRY(ua_lss_validate(B, N, H, D, P));
+  if (!bytes) return fail(UA_ERR_INVALID_ARG, "bytes is NULL");
+  *bytes = plan_lss_rank(make_shape(B, N, H, D, P)).total;
+  return UA_OK;
+}
+
+ua_status ua_lss_rank_bwd(const void* q, const void* k_full, const void* v_full, const void* out, const float* lse,
+                          const void* dout, void* dq, float* dk_part, float* dv_part, int64_t B, int64_t N, int H,
+                          int D, int P, int deterministic, void* workspace, size_t workspace_bytes,
+                          ua_stream_t stream) {
+  UA_TRY(ua_lss_validate(B, N, H, D, P));
+  UA_TRY(check_ptrs({q, k_full, v_full, out, lse, dout, dq, dk_part, dv_part, workspace}));
+  const Shape s = make_shape(B, N, H, D, P);
+  if (workspace_bytes < plan_lss_rank(s).total)
+    return fail(UA_ERR_INVALID_ARG, "workspace too small: need %zu bytes, got %zu", plan_lss_rank(s).total,
+                workspace_bytes);
+  UA_TRY(check_device());
+  UA_TRY(check_async(nullptr));
+  return lss_rank_bwd(nullptr, s, q, k_full, v_full, out, lse, dout, dq, dk_part, dv_part, deterministic ? 1 : 0,
+                      static_cast<char*>(workspace), reinterpret_cast<cudaStream_t>(stream));
 }
 
 ua_status ua_ctx_enable_timing(ua_ctx* ctx, int enable) {

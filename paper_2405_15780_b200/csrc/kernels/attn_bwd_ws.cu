@@ -69,6 +69,9 @@
 #ifndef UA_BWD_PAIR
 #define UA_BWD_PAIR 1       // clusters of 2 CTAs on adjacent key tiles of a head sharing each Q / dO half tile (TMA multicast)
 #endif
+#ifndef UA_BWD_DET_SLOTS
+#define UA_BWD_DET_SLOTS 1  // dQ-less (deterministic) variant: no dS^T / staging buffers, their smem as ring slots
+#endif
 #ifndef UA_BWD_STAGGER
 #define UA_BWD_STAGGER 16   // query-tile window the persistent CTAs' start tiles are spread over
 #endif
@@ -77,7 +80,7 @@ namespace ua {
 
 namespace {
 
-template <int D>
+template <int D, bool kDq = true>
 struct BwdWsCfg {
   using G = TileGeom<D>;
   static constexpr int kThreads = 512;
@@ -90,12 +93,17 @@ struct BwdWsCfg {
   static constexpr bool kKvTmem = UA_BWD_KV_TMEM && D <= 64;
   static constexpr uint32_t kColK = 256 + 3 * D, kColV = 256 + 3 * D + D / 2;
   static constexpr int kHalfBytes = 64 * D * 2;               // one [64][D] bf16 half tile
-  // half-tile ring depth; UA_BWD_BOX2 trades one D <= 64 slot for a second dQ staging box
-  static constexpr int kSlots = D == 128 ? 3 : (D == 80 ? 4 : (UA_BWD_BOX2 && D == 64 ? 5 : 6));
+  // half-tile ring depth; UA_BWD_BOX2 trades one D == 64 slot for a second dQ staging box.
+  // kDq = false (deterministic mode) with UA_BWD_DET_SLOTS: no dS^T or dQ staging buffers, their
+  // shared memory goes to the ring (A/B at c4 and N = 32K: neutral, 795 vs 798 and 809 vs 811 TFLOP/s).
+  static constexpr bool kDqBufs = kDq || !UA_BWD_DET_SLOTS;
+  static constexpr int kSlots =
+      !kDqBufs ? (D == 128 ? 4 : 8) : (D == 128 ? 3 : (D == 80 ? 4 : (UA_BWD_BOX2 && D == 64 ? 5 : 6)));
   static constexpr int kSlotBytes = 2 * kHalfBytes;            // Q_h + dO_h
-  static constexpr int kNumDs = kAliasDq ? 1 : 2;              // dS^T smem buffers
+  static constexpr int kNumDs = !kDqBufs ? 0 : (kAliasDq ? 1 : 2);   // dS^T smem buffers
   static constexpr int kDsBytes = 128 * 128 * 2;
-  static constexpr int kStageBoxes = (D == 128 || (UA_BWD_BOX2 && D == 64)) ? 2 : 1;  // 16 KB fp32 staging boxes for dQ
+  static constexpr int kStageBoxes =   // 16 KB fp32 staging boxes for dQ
+      !kDqBufs ? 0 : ((D == 128 || (UA_BWD_BOX2 && D == 64)) ? 2 : 1);
   static constexpr int kBoxBytes = 128 * 32 * 4;
   static constexpr int kLsedBytes = 128 * 4;                   // per slot: 64 x -lse*log2e, 64 x -Delta
   static constexpr bool kPolyExp = UA_BWD_POLY_MOD > 0;
@@ -131,7 +139,7 @@ __host__ __device__ constexpr int ws_threads() {
 // attn_bwd_dq_kernel (attn_bwd_dq.cu), so no dS^T staging, dQ GEMM or reduction here.
 template <int D, bool kDq>
 __global__ void __launch_bounds__(ws_threads<D, kDq>(), 1) attn_bwd_ws_kernel(const __grid_constant__ BwdParams p) {
-  using C = BwdWsCfg<D>;
+  using C = BwdWsCfg<D, kDq>;
   constexpr bool kAlias = C::kAliasDq && kDq;   // dQ shares TMEM with dP^T (D = 128)
   constexpr bool kSepP = ws_sep_p<D, kDq>();
   constexpr bool kSplit = kSepP || ws_ew_split<D, kDq>();   // two elementwise warpgroups per half
@@ -768,7 +776,7 @@ __global__ void __launch_bounds__(ws_threads<D, kDq>(), 1) attn_bwd_ws_kernel(co
 
 template <int D, bool kDq>
 cudaError_t launch_bwd_ws_impl(const BwdParams& p, cudaStream_t stream) {
-  using C = BwdWsCfg<D>;
+  using C = BwdWsCfg<D, kDq>;
   const int num_sms = current_num_sms();
   if (num_sms <= 0) return cudaErrorNoDevice;
   cudaError_t e = set_max_smem(attn_bwd_ws_kernel<D, kDq>, C::kSmemBytes);

@@ -45,7 +45,8 @@ inline bool make_tmap_bf16_4d(CUtensorMap* m, const void* base, const uint64_t d
 // 2-D bf16 tensor map {cols, rows} over a row-major [rows][cols] matrix with
 // leading dimension ld (elements), box {box0, box1}, SWIZZLE_128B (box0 * 2 <= 128).
 inline bool make_tmap_bf16_2d(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows, uint64_t ld,
-                              uint32_t box0, uint32_t box1) {
+                              uint32_t box0, uint32_t box1,
+                              CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   EncodeTiledFn fn = encode_tiled_fn();
   if (!fn) return false;
   cuuint64_t gd[2] = {cols, rows};
@@ -53,7 +54,7 @@ inline bool make_tmap_bf16_2d(CUtensorMap* m, const void* base, uint64_t cols, u
   cuuint32_t box[2] = {box0, box1};
   cuuint32_t es[2] = {1, 1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), gd, gs, box, es,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }

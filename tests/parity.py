@@ -55,7 +55,8 @@ def gate_out(x, ref, gate_a=True, absv=None, atol_max=1e-2, atol_mean=1e-3):
         bound = 1e-3 + 2.0 ** -6 * np.abs(ref)
     elt = err - bound
     stats = dict(max=float(err.max()), mean=float(err.mean()), rel_l2=r, elt_margin=float((err / bound).max()),
-                 gate_a_max_frac=float(err.max() / atol_max) if gate_a else None)
+                 gate_a_max_frac=float(err.max() / atol_max) if gate_a else None,
+                 q7_margin=float((err / (1e-3 + 2.0 ** -6 * np.abs(ref))).max()))
     _log("out", stats)
     assert elt.max() <= 0, f"elementwise gate exceeded by {elt.max():.3e}"
     return stats
@@ -78,7 +79,8 @@ def gate_grad(x, ref, gate_a=True, gabs=None, atol_max=2e-2, rel=1e-2, elt_atol=
     scale = (np.abs(gabs) + np.abs(ref)) * 2.0 * 2.0 ** -8 if gabs is not None else 2.0 ** -6 * np.abs(ref)
     elt = err - (elt_atol + scale)
     _log("grad", dict(max=float(err.max()), rel_l2=r, elt_margin=float((err / (elt_atol + scale)).max()),
-                      gate_a_max_frac=float(err.max() / atol_max) if gate_a else None))
+                      gate_a_max_frac=float(err.max() / atol_max) if gate_a else None,
+                      q7_margin=float((err / (1e-3 + 2.0 ** -6 * np.abs(ref))).max())))
     assert elt.max() <= 0, f"elementwise gate exceeded by {elt.max():.3e}"
     if gate_a:
         assert err.max() <= atol_max, f"max-abs {err.max():.3e} > {atol_max}"
