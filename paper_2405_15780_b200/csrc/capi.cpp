@@ -65,7 +65,9 @@ size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
-ua_status check_device() {
+}  // namespace
+
+ua_status ua_internal::check_device() {
   static std::mutex mu;
   static int checked[64] = {0};  // 0 unknown, 1 ok, 2 bad
   int dev = -1;
@@ -85,6 +87,9 @@ ua_status check_device() {
   if (checked[dev] != 1) return fail(UA_ERR_UNSUPPORTED, "device %d is not sm_100 (B200); kernels are sm_100a only", dev);
   return UA_OK;
 }
+
+namespace {
+using ua_internal::check_device;
 
 struct Shape {
   int64_t B, N, Nl;

@@ -61,6 +61,8 @@ namespace ua_internal {
 ua_status fail(ua_status s, const char* fmt, ...);
 // Releases per-ctx state of the projection layer (layer.cpp; none at present); called by ua_ctx_destroy.
 void layer_release(ua_ctx* ctx);
+// UA_OK if the current device is an sm_100 GPU, else UA_ERR_UNSUPPORTED (no CPU fallback).
+ua_status check_device();
 }  // namespace ua_internal
 
 #define UA_CUDA(expr)                                                                                    \

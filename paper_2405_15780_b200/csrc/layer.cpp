@@ -110,6 +110,7 @@ ua_status gemm(bool a_mn, bool b_mn, int64_t M, int64_t N, int64_t K, std::initi
   p.nseg = int(As.size());
   p.a_mn = a_mn;
   p.b_mn = b_mn;
+  UA_TRY(ua_internal::check_device());
   UA_CUDA(ua::launch_gemm(p, stream));
   return UA_OK;
 }

@@ -176,3 +176,18 @@ def test_head_attn_bwd_workspace_size():
     _, b1 = ua.workspace_size(B, N, H, D, 1)
     assert ua.lib().ua_head_attn_bwd_workspace_size(B, N, H, D, 1, ctypes.byref(n)) == 0
     assert b1 >= n.value + B * N * H * 4
+
+
+def test_gemm_validates_before_launch():
+    """ua_gemm_bf16 checks segment counts, pointers and 16-byte row alignment on the host."""
+    import ctypes
+    L = ua.lib()
+    arr = (ctypes.c_void_p * 3)(256, 512, 768)
+    c = ctypes.c_void_p(1024)
+    assert L.ua_gemm_bf16(0, 0, 128, 128, 64, arr, arr, 0, c, 0, None) == 1      # nseg = 0
+    assert L.ua_gemm_bf16(0, 0, 128, 128, 64, arr, arr, 4, c, 0, None) == 1      # nseg > 3
+    assert L.ua_gemm_bf16(0, 0, 128, 128, 60, arr, arr, 1, c, 0, None) == 1      # K-major rows of 60 bf16
+    assert L.ua_gemm_bf16(1, 1, 100, 128, 64, arr, arr, 1, c, 0, None) == 1      # MN-major A with M = 100
+    bad = (ctypes.c_void_p * 1)(258)
+    assert L.ua_gemm_bf16(0, 0, 128, 128, 64, bad, arr, 1, c, 0, None) == 1      # misaligned A
+    assert L.ua_gemm_bf16(0, 0, 0, 128, 64, arr, arr, 1, c, 0, None) == 1        # M = 0
