@@ -156,7 +156,12 @@ def load_ncu(kind, D, N, P, det=False):
         return None
     try:
         d = json.load(open(path))
-        return d.get(f"{kind}{'_det' if det else ''}_D{D}_N{N}_P{P}")
+        key = f"{kind}{'_det' if det else ''}_D{D}_N{N}"
+        if f"{key}_P{P}" in d:
+            return d[f"{key}_P{P}"]
+        if f"{key}_P1" in d:   # the per-rank kernel at P > 1 is the same kernel on H/P heads
+            return dict(d[f"{key}_P1"], note=f"P = 1 capture; at P = {P} each rank runs the same kernel on H/P heads")
+        return None
     except Exception:
         return None
 
