@@ -345,14 +345,14 @@ def main():
     kf = kstats("attn_fwd", fwd_f)
     ncu_b = None if lss or B != 1 else load_ncu("attn_bwd", D, N, P, args.deterministic)
     ncu_f = None if lss or B != 1 else load_ncu("attn_fwd", D, N, P)
-    traffic = ncu_b.get("dram_bytes") if ncu_b else None
+    traffic = ncu_b.get("dram_bytes") if (ncu_b and "note" not in ncu_b) else None   # per launch, this shape only
     roofline = {"bound": "tensor", "kernel": "attn_bwd_kernel", "achieved": kb["tflops"],
                 "peak": peaks["bf16_sustained"], "unit": UNIT, "frac": kb["tflops"] / peaks["bf16_sustained"],
                 "frac_of_burst": kb["tflops"] / peaks["bf16_burst"], "peak_source": peaks["source"] + " sustained",
                 "traffic": traffic, "traffic_source": ncu_b.get("source") if ncu_b else None,
                 "flops_per_launch": bwd_f / P, "flops_formula": "10*B*N^2*(H/P)*D per launch (5 GEMMs incl. recompute)"}
     fwd_roof = {"kernel": "attn_fwd_kernel", "achieved": kf["tflops"], "frac": kf["tflops"] / peaks["bf16_sustained"],
-                "avg_ms": kf["avg_ms"], "traffic": ncu_f.get("dram_bytes") if ncu_f else None}
+                "avg_ms": kf["avg_ms"], "traffic": ncu_f.get("dram_bytes") if (ncu_f and "note" not in ncu_f) else None}
     ncu = {"attn_bwd": ncu_b, "attn_fwd": ncu_f,
            "note": "from the committed ncu --set full captures named in each entry's source (not this run)"}
     # our kernels per phase call: attn_bwd = bwd_prep + the backward kernel (+ the dQ kernel in
