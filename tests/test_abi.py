@@ -191,3 +191,14 @@ def test_gemm_validates_before_launch():
     bad = (ctypes.c_void_p * 1)(258)
     assert L.ua_gemm_bf16(0, 0, 128, 128, 64, bad, arr, 1, c, 0, None) == 1      # misaligned A
     assert L.ua_gemm_bf16(0, 0, 0, 128, 64, arr, arr, 1, c, 0, None) == 1        # M = 0
+
+
+def test_no_vendor_blas_linked():
+    """The projection GEMMs run on the library's own tcgen05 kernel: the
+    shared object links NCCL and the CUDA runtime only, no cuBLAS / cuBLASLt."""
+    import subprocess
+    out = subprocess.run(["readelf", "-d", ua.LIB_PATH], capture_output=True, text=True).stdout
+    needed = [line for line in out.splitlines() if "(NEEDED)" in line]
+    assert needed and not any("cublas" in line.lower() for line in needed), needed
+    syms = subprocess.run(["nm", "-D", "--undefined-only", ua.LIB_PATH], capture_output=True, text=True).stdout
+    assert "cublas" not in syms.lower()
