@@ -10,8 +10,10 @@ P:166; R14); rank 0 gathers and checks:
   * the collective law: 1 call in the forward (all-gather K, V), 2 in the
     backward (all-gather K, V; reduce-scatter dK, dV) and their byte counts;
   * P > H runs (no head limit).
-Prints "LSS_OK" on success."""
+Prints "LSS_OK" on success of each case; --cases '<json list of {B,N,H,D,sigma,det}>' runs
+several cases in one process group."""
 import argparse
+import json
 import os
 import sys
 
@@ -28,20 +30,7 @@ import synth  # noqa: E402
 from tests.parity import gate_grad, gate_lse, gate_out  # noqa: E402
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--B", type=int, default=1)
-    ap.add_argument("--N", type=int, default=4096)
-    ap.add_argument("--H", type=int, default=8)
-    ap.add_argument("--D", type=int, default=64)
-    ap.add_argument("--sigma", type=float, default=1.0)
-    ap.add_argument("--det", type=int, default=0, help="deterministic backward: dq also bitwise reproducible")
-    a = ap.parse_args()
-    rank, P = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
-    local = int(os.environ.get("LOCAL_RANK", rank))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    dist.init_process_group("nccl", device_id=dev)
+def run_case(a, P, rank, local, dev):
     B, N, H, D = a.B, a.N, a.H, a.D
     Nl = N // P
     q, k, v, do = synth.qkv(B, N, H, D, seed=91, sigma_qk=a.sigma, with_do=True)
@@ -94,6 +83,7 @@ def main():
             y = y.float().cpu().numpy()
             assert (np.abs(x - y) - (2e-2 + 2.0 ** -7 * np.abs(y))).max() <= 0
         f64 = [synth.to_f64(t) for t in (q, k, v, do)]
+        oracle.set_num_threads(len(os.sched_getaffinity(0)))   # torchrun sets OMP_NUM_THREADS=1 per rank
         ref, ref_lse, absv = oracle.attn_fwd(*f64[:3], with_abs=True)
         gate_out(out_g, ref, gate_a=a.sigma == 1.0, absv=absv)
         gate_lse(lse_g, ref_lse)
@@ -101,9 +91,29 @@ def main():
         for x, y, gb in zip((dq_g, dk_g, dv_g), (rdq, rdk, rdv), gabs):
             gate_grad(x, y, gate_a=a.sigma == 1.0, gabs=gb)
         c1ctx.close()
-        print("LSS_OK", flush=True)
+        print("LSS_OK", vars(a), flush=True)
     ctx.close()
     dist.barrier()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--B", type=int, default=1)
+    ap.add_argument("--N", type=int, default=4096)
+    ap.add_argument("--H", type=int, default=8)
+    ap.add_argument("--D", type=int, default=64)
+    ap.add_argument("--sigma", type=float, default=1.0)
+    ap.add_argument("--det", type=int, default=0, help="deterministic backward: dq also bitwise reproducible")
+    ap.add_argument("--cases", default="", help="JSON list of per-case overrides of the options above")
+    a = ap.parse_args()
+    rank, P = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    base = {k: v for k, v in vars(a).items() if k != "cases"}
+    for c in (json.loads(a.cases) if a.cases else [{}]):
+        run_case(argparse.Namespace(**{**base, **c}), P, rank, local, dev)
     dist.destroy_process_group()
 
 

@@ -7,8 +7,10 @@ through the C ABI with P ranks; rank 0 gathers and checks:
   * the all-to-all call law: 2 in the forward, 2 in the backward (P:425, S:250);
   * an invalid shape (head limit) fails identically on every rank
     before any collective (no hang).
-Prints "MP_OK" on success."""
+Prints "MP_OK" on success of each case; --cases '<json list of {N,H,D,sigma,mode,det}>' runs
+several cases in one process group (one launch per P in the test suite)."""
 import argparse
+import json
 import os
 import sys
 
@@ -25,20 +27,7 @@ import synth  # noqa: E402
 from tests.parity import gate_grad, gate_lse, gate_out  # noqa: E402
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--N", type=int, default=4096)
-    ap.add_argument("--H", type=int, default=8)
-    ap.add_argument("--D", type=int, default=64)
-    ap.add_argument("--sigma", type=float, default=1.0)
-    ap.add_argument("--mode", default="nccl", choices=["nccl", "peer"])
-    ap.add_argument("--det", type=int, default=0, help="deterministic backward: P-way grads == P=1 grads bitwise")
-    a = ap.parse_args()
-    rank, P = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
-    local = int(os.environ.get("LOCAL_RANK", rank))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    dist.init_process_group("nccl", device_id=dev)
+def run_case(a, P, rank, local, dev):
     B, N, H, D = 1, a.N, a.H, a.D
     Nl = N // P
     q, k, v, do = synth.qkv(B, N, H, D, seed=77, sigma_qk=a.sigma, with_do=True)
@@ -102,6 +91,7 @@ def main():
             else:
                 assert np.abs(x - y.float().cpu().numpy()).max() <= 2e-2
         f64 = [synth.to_f64(t) for t in (q, k, v, do)]
+        oracle.set_num_threads(len(os.sched_getaffinity(0)))   # torchrun sets OMP_NUM_THREADS=1 per rank
         ref, ref_lse, absv = oracle.attn_fwd(*f64[:3], with_abs=True)
         gate_out(out_g, ref, gate_a=a.sigma == 1.0, absv=absv)
         gate_lse(lse_g, ref_lse)
@@ -109,9 +99,29 @@ def main():
         for x, y, gb in zip((dq_g, dk_g, dv_g), (rdq, rdk, rdv), gabs):
             gate_grad(x, y, gate_a=a.sigma == 1.0, gabs=gb)
         c1ctx.close()
-        print("MP_OK", flush=True)
+        print("MP_OK", vars(a), flush=True)
     ctx.close()
     dist.barrier()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--N", type=int, default=4096)
+    ap.add_argument("--H", type=int, default=8)
+    ap.add_argument("--D", type=int, default=64)
+    ap.add_argument("--sigma", type=float, default=1.0)
+    ap.add_argument("--mode", default="nccl", choices=["nccl", "peer"])
+    ap.add_argument("--det", type=int, default=0, help="deterministic backward: P-way grads == P=1 grads bitwise")
+    ap.add_argument("--cases", default="", help="JSON list of per-case overrides of the options above")
+    a = ap.parse_args()
+    rank, P = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    base = {k: v for k, v in vars(a).items() if k != "cases"}
+    for c in (json.loads(a.cases) if a.cases else [{}]):
+        run_case(argparse.Namespace(**{**base, **c}), P, rank, local, dev)
     dist.destroy_process_group()
 
 

@@ -20,9 +20,16 @@ def torchrun(nproc, script, *args, timeout=900, env=None):
 
 
 # ----------------------------------------------------------------- GPU, NCCL
-@pytest.mark.gpu
-@pytest.mark.parametrize("mode", ["nccl", "peer"])
-@pytest.mark.parametrize("P,N,H,D,sigma", [
+# One torchrun launch per world size runs every case of that size in one process group
+# (process start-up, CUDA / NCCL initialisation and the import of torch are paid once);
+# each case prints its own OK line.  The full-size matrix (every BASELINE config at every P
+# and transport) runs with UA_MGPU_FULL=1; by default a representative subset runs.
+import json  # noqa: E402
+
+FULL = os.environ.get("UA_MGPU_FULL", "0") == "1"
+
+ULYSSES_CASES = [
+    # P, N, H, D, sigma
     (2, 4096, 8, 64, 1.0),
     (2, 2048, 4, 128, 2.0),
     (2, 4050, 4, 64, 1.0),      # ragged per-rank tail: N/P = 2025
@@ -30,98 +37,87 @@ def torchrun(nproc, script, *args, timeout=900, env=None):
     (8, 8192, 16, 64, 1.0),
     (8, 2048, 8, 32, 2.0),
     (2, 2048, 4, 72, 1.0),      # D=72 (peer transport: Delta in its own push pass)
-])
-def test_ulysses_p_way(P, N, H, D, sigma, mode):
-    if torch.cuda.device_count() < P:
-        pytest.skip(f"needs {P} GPUs")
-    r = torchrun(P, os.path.join(ROOT, "tests", "mp_ulysses_check.py"), f"--N={N}", f"--H={H}", f"--D={D}",
-                 f"--sigma={sigma}", f"--mode={mode}")
-    assert r.returncode == 0 and "MP_OK" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
-
-
-@pytest.mark.gpu
-@pytest.mark.parametrize("mode", ["nccl", "peer"])
-@pytest.mark.parametrize("P,N,H,D,sigma", [
+]
+ULYSSES_DET_CASES = [
     (2, 4096, 8, 64, 1.0),
     (2, 2050, 4, 128, 2.0),     # ragged: N/P = 1025
     (4, 4096, 8, 32, 2.0),
     (8, 8192, 16, 64, 1.0),
-])
-def test_ulysses_p_way_deterministic(P, N, H, D, sigma, mode):
-    """Deterministic backward: P-way dq, dk, dv bitwise equal to P = 1."""
+]
+LSS_CASES = [
+    # P, B, N, H, D, sigma, det
+    (2, 1, 4096, 8, 64, 1.0, 0),
+    (2, 1, 2048, 4, 128, 2.0, 0),
+    (2, 1, 4050, 4, 64, 1.0, 0),     # ragged segment: N/P = 2025
+    (2, 2, 2048, 4, 64, 1.0, 0),     # B > 1: K, V re-laid [Nl][B][H][D] before the gather
+    (4, 1, 4096, 2, 64, 1.0, 0),     # P > H: no head limit
+    (4, 1, 4096, 8, 32, 2.0, 0),
+    (8, 1, 8192, 4, 64, 1.0, 0),
+    (2, 1, 2048, 3, 72, 2.0, 0),     # D=72
+    (2, 1, 4096, 8, 64, 1.0, 1),     # deterministic backward
+    (4, 2, 2048, 2, 128, 1.0, 1),
+]
+LAYER_CASES = [(2, 1024, 4, 64), (4, 2048, 8, 64), (2, 600, 2, 72)]
+
+
+def run_cases(P, script, ok, cases, timeout=1500):
+    if not cases:
+        pytest.skip(f"no cases at P={P}")
     if torch.cuda.device_count() < P:
         pytest.skip(f"needs {P} GPUs")
-    r = torchrun(P, os.path.join(ROOT, "tests", "mp_ulysses_check.py"), f"--N={N}", f"--H={H}", f"--D={D}",
-                 f"--sigma={sigma}", f"--mode={mode}", "--det=1")
-    assert r.returncode == 0 and "MP_OK" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
+    r = torchrun(P, os.path.join(ROOT, "tests", script), f"--cases={json.dumps(cases)}", timeout=timeout)
+    assert r.returncode == 0 and r.stdout.count(ok) == len(cases), r.stdout[-3000:] + r.stderr[-3000:]
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("P,B,N,H,D,sigma", [
-    (2, 1, 4096, 8, 64, 1.0),
-    (2, 1, 2048, 4, 128, 2.0),
-    (2, 1, 4050, 4, 64, 1.0),     # ragged segment: N/P = 2025
-    (2, 2, 2048, 4, 64, 1.0),     # B > 1: K, V re-laid [Nl][B][H][D] before the gather
-    (4, 1, 4096, 2, 64, 1.0),     # P > H: no head limit (P:317)
-    (4, 1, 4096, 8, 32, 2.0),
-    (8, 1, 8192, 4, 64, 1.0),
-    (2, 1, 2048, 3, 72, 2.0),     # D=72
-])
-def test_lss_p_way(P, B, N, H, D, sigma):
-    if torch.cuda.device_count() < P:
-        pytest.skip(f"needs {P} GPUs")
-    r = torchrun(P, os.path.join(ROOT, "tests", "mp_lss_check.py"), f"--B={B}", f"--N={N}", f"--H={H}", f"--D={D}",
-                 f"--sigma={sigma}")
-    assert r.returncode == 0 and "LSS_OK" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
+@pytest.mark.parametrize("P", [2, 4, 8])
+def test_ulysses_p_way(P):
+    """Every Ulysses case at this P, both transports, default and deterministic backward:
+    P-way forward == P = 1 bitwise, deterministic P-way grads == P = 1 bitwise,
+    oracle gates, call / byte law, head-limit error on every rank without a hang."""
+    cases = [dict(N=N, H=H, D=D, sigma=s, mode=m, det=0) for (p, N, H, D, s) in ULYSSES_CASES if p == P
+             for m in ("nccl", "peer")]
+    cases += [dict(N=N, H=H, D=D, sigma=s, mode=m, det=1) for (p, N, H, D, s) in ULYSSES_DET_CASES if p == P
+              for m in ("nccl", "peer")]
+    run_cases(P, "mp_ulysses_check.py", "MP_OK", cases)
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("P,B,N,H,D", [(2, 1, 4096, 8, 64), (4, 2, 2048, 2, 128)])
-def test_lss_p_way_deterministic(P, B, N, H, D):
-    """LSS with the deterministic backward: oracle gates, dq bitwise run to run."""
-    if torch.cuda.device_count() < P:
-        pytest.skip(f"needs {P} GPUs")
-    r = torchrun(P, os.path.join(ROOT, "tests", "mp_lss_check.py"), f"--B={B}", f"--N={N}", f"--H={H}", f"--D={D}",
-                 "--sigma=1.0", "--det=1")
-    assert r.returncode == 0 and "LSS_OK" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
+@pytest.mark.parametrize("P", [2, 4, 8])
+def test_lss_p_way(P):
+    """Every LSS case at this P: bitwise P-way == P = 1 forward, oracle gates, collective law."""
+    cases = [dict(B=B, N=N, H=H, D=D, sigma=s, det=d) for (p, B, N, H, D, s, d) in LSS_CASES if p == P]
+    run_cases(P, "mp_lss_check.py", "LSS_OK", cases)
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("P,N,H,D", [(2, 1024, 4, 64), (4, 2048, 8, 64), (2, 600, 2, 72)])
-def test_layer_p_way(P, N, H, D):
+@pytest.mark.parametrize("P", [2, 4])
+def test_layer_p_way(P):
     """Attention layer: projections + Ulysses + the weight-gradient all-reduce."""
-    if torch.cuda.device_count() < P:
-        pytest.skip(f"needs {P} GPUs")
-    r = torchrun(P, os.path.join(ROOT, "tests", "mp_layer_check.py"), f"--N={N}", f"--H={H}", f"--D={D}")
-    assert r.returncode == 0 and "LAYER_OK" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
+    cases = [dict(N=N, H=H, D=D) for (p, N, H, D) in LAYER_CASES if p == P]
+    run_cases(P, "mp_layer_check.py", "LAYER_OK", cases)
+
+
+BIG_DEFAULT = [("c3", 1, "nccl", 0), ("c4", 1, "nccl", 0), ("c4", 2, "nccl", 0), ("c3", 4, "peer", 0),
+               ("c4", 4, "nccl", 1), ("c5", 8, "nccl", 0)]
+BIG_FULL = [("c3", 2, "nccl", 0), ("c3", 4, "nccl", 0), ("c3", 8, "nccl", 0), ("c4", 4, "nccl", 0),
+            ("c4", 8, "nccl", 0), ("c5", 4, "nccl", 0), ("c4", 4, "peer", 0), ("c5", 4, "peer", 0),
+            ("c4", 8, "peer", 0), ("c5", 8, "peer", 0), ("c4", 1, "nccl", 1), ("c3", 2, "nccl", 1),
+            ("c5", 4, "nccl", 1)]
 
 
 @pytest.mark.gpu
 @pytest.mark.slow
-@pytest.mark.parametrize("config,P,mode", [("c3", 1, "nccl"), ("c4", 1, "nccl"),
-                                           ("c3", 2, "nccl"), ("c3", 4, "nccl"), ("c3", 8, "nccl"),
-                                           ("c4", 2, "nccl"), ("c4", 4, "nccl"), ("c4", 8, "nccl"),
-                                           ("c5", 4, "nccl"), ("c5", 8, "nccl"),
-                                           ("c3", 4, "peer"), ("c4", 4, "peer"), ("c5", 4, "peer"),
-                                           ("c4", 8, "peer"), ("c5", 8, "peer")])
-def test_bigconfig_p_way(config, P, mode):
-    """BASELINE configs at full size: sampled-row oracle parity + invariants."""
+@pytest.mark.parametrize("config,P,mode,det", BIG_DEFAULT + BIG_FULL)
+def test_bigconfig_p_way(config, P, mode, det):
+    """BASELINE configs at full size: sampled-row oracle parity (out, lse, dQ; dK / dV key rows at
+    c3 for P > 1) + invariants.  The BIG_FULL cases run with UA_MGPU_FULL=1."""
+    if (config, P, mode, det) in BIG_FULL and not FULL:
+        pytest.skip("full-size matrix: UA_MGPU_FULL=1")
     if torch.cuda.device_count() < P:
         pytest.skip(f"needs {P} GPUs")
     r = torchrun(P, os.path.join(ROOT, "tests", "mp_bigconfig_check.py"), f"--config={config}", f"--mode={mode}",
-                 timeout=1500)
-    assert r.returncode == 0 and "BIG_OK" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
-
-
-@pytest.mark.gpu
-@pytest.mark.slow
-@pytest.mark.parametrize("config,P", [("c4", 1), ("c3", 2), ("c4", 4), ("c5", 4)])
-def test_bigconfig_deterministic(config, P):
-    """Full-size configs with the deterministic backward: sampled-row oracle parity + invariants."""
-    if torch.cuda.device_count() < P:
-        pytest.skip(f"needs {P} GPUs")
-    r = torchrun(P, os.path.join(ROOT, "tests", "mp_bigconfig_check.py"), f"--config={config}", "--det=1",
-                 timeout=1500)
+                 f"--det={det}", timeout=1500)
     assert r.returncode == 0 and "BIG_OK" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
 
 
