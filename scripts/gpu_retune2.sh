@@ -1,0 +1,5 @@
+set -x
+V=paper_2405_15780_b200/variants
+L=paper_2405_15780_b200/libulysses_attn.so
+timeout 1200 python scripts/ab.py --what bwd --rounds 4 --N 188416 --libs $L $V/libpoly2.so $V/libpoly3.so $V/libpoly5.so 2>&1 | tail -5
+timeout 600 python scripts/ab.py --what bwd --rounds 6 --libs $L $V/libpoly2.so $V/libpoly3.so $V/libpoly5.so 2>&1 | tail -5
