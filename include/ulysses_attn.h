@@ -120,9 +120,10 @@ ua_status ua_ctx_enable_timing(ua_ctx* ctx, int enable);
  *               NVLink, and the attention epilogues (O forward; dK, dV and the
  *               dQ finaliser backward) store each row straight into the token
  *               owner's buffer; completion is a system-scope flag per peer.
- *               The receive buffers are library-owned device memory, CUDA-IPC
- *               mapped on every rank (allocated on first use per shape; the
- *               handles travel over the ctx's NCCL communicator).
+ *               The receive buffers are library-owned NCCL symmetric memory
+ *               (ncclMemAlloc + ncclCommWindowRegister, collective, on first
+ *               use per shape), addressed on every rank through the window's
+ *               load/store-accessible peer pointers (NCCL >= 2.28).
  * Collective: every rank sets the same mode before its next call.
  * UA_ERR_UNSUPPORTED if P == 1 or the peer mappings cannot be created. */
 enum { UA_A2A_NCCL = 0, UA_A2A_PEER = 1 };

@@ -332,43 +332,34 @@ ua_status launch_attention_bwd(const void* q, const void* k, const void* v, cons
 }
 
 // ------------------------------------------------------------ peer all-to-all
-// Collective: exchange CUDA IPC handles of `pb.local` through the ctx's NCCL
-// communicator and open every peer's copy (the buffers are library-owned, so
-// the mapping is done once per shape, not per call).
-ua_status peer_exchange(ua_ctx* ctx, ua_ctx::PeerBuf& pb, cudaStream_t stream) {
-  cudaIpcMemHandle_t mine;
-  UA_CUDA(cudaIpcGetMemHandle(&mine, pb.local));
+// Library-owned receive buffers in NCCL symmetric memory: allocated with ncclMemAlloc, registered
+// collectively as a window (NCCL_WIN_COLL_SYMMETRIC), and every rank's copy addressed through the
+// window's load/store-accessible peer pointers (once per shape, not per call).
+ua_status peer_map(ua_ctx* ctx, ua_ctx::PeerBuf& pb, cudaStream_t stream) {
+  UA_NCCL(ncclCommWindowRegister(ctx->comm, pb.local, pb.bytes, &pb.win, NCCL_WIN_COLL_SYMMETRIC));
   const int P = ctx->P;
-  char* d = nullptr;
-  UA_CUDA(cudaMalloc(&d, sizeof(cudaIpcMemHandle_t) * (P + 1)));
-  UA_CUDA(cudaMemcpyAsync(d + sizeof(mine) * P, &mine, sizeof(mine), cudaMemcpyHostToDevice, stream));
-  UA_NCCL(ncclAllGather(d + sizeof(mine) * P, d, sizeof(mine), ncclUint8, ctx->comm, stream));
-  std::vector<cudaIpcMemHandle_t> all(P);
-  UA_CUDA(cudaMemcpyAsync(all.data(), d, sizeof(mine) * P, cudaMemcpyDeviceToHost, stream));
+  void** d = nullptr;
+  UA_CUDA(cudaMalloc(reinterpret_cast<void**>(&d), sizeof(void*) * P));
+  UA_CUDA(ua_internal::launch_lsa_ptrs(pb.win, P, d, stream));
+  UA_CUDA(cudaMemcpyAsync(pb.peer, d, sizeof(void*) * P, cudaMemcpyDeviceToHost, stream));
   UA_CUDA(cudaStreamSynchronize(stream));
   cudaFree(d);
-  for (int k = 0; k < P; ++k) {
-    if (k == ctx->rank) {
-      pb.peer[k] = pb.local;
-    } else {
-      UA_CUDA(cudaIpcOpenMemHandle(&pb.peer[k], all[k], cudaIpcMemLazyEnablePeerAccess));
-    }
-  }
+  for (int k = 0; k < P; ++k)
+    if (!pb.peer[k]) return fail(UA_ERR_NCCL, "NCCL window: no load/store pointer for rank %d", k);
   return UA_OK;
 }
 
 void peer_release(ua_ctx* ctx, ua_ctx::PeerBuf& pb) {
-  for (int k = 0; k < ctx->P; ++k)
-    if (k != ctx->rank && pb.peer[k]) cudaIpcCloseMemHandle(pb.peer[k]);
-  if (pb.local) cudaFree(pb.local);
+  if (pb.win) ncclCommWindowDeregister(ctx->comm, pb.win);
+  if (pb.local) ncclMemFree(pb.local);
   pb = ua_ctx::PeerBuf();
 }
 
 // Collective (all ranks call with the same shape): make sure `pb` holds at
-// least `bytes`, re-allocating and re-mapping when it grows.
+// least `bytes`, re-allocating and re-registering when it grows.
 ua_status peer_ensure(ua_ctx* ctx, ua_ctx::PeerBuf& pb, size_t bytes, cudaStream_t stream) {
   if (pb.local && pb.bytes >= bytes) return UA_OK;
-  // every rank has drained its previous steps before anyone unmaps / frees
+  // every rank has drained its previous steps before anyone deregisters / frees
   UA_CUDA(cudaDeviceSynchronize());
   int* dummy = nullptr;
   UA_CUDA(cudaMalloc(&dummy, sizeof(int)));
@@ -376,10 +367,12 @@ ua_status peer_ensure(ua_ctx* ctx, ua_ctx::PeerBuf& pb, size_t bytes, cudaStream
   UA_CUDA(cudaStreamSynchronize(stream));
   cudaFree(dummy);
   peer_release(ctx, pb);
-  UA_CUDA(cudaMalloc(&pb.local, bytes));
+  const size_t align = NCCL_WIN_REQUIRED_ALIGNMENT;
+  bytes = (bytes + align - 1) / align * align;
+  UA_NCCL(ncclMemAlloc(&pb.local, bytes));
   UA_CUDA(cudaMemset(pb.local, 0, bytes));
   pb.bytes = bytes;
-  return peer_exchange(ctx, pb, stream);
+  return peer_map(ctx, pb, stream);
 }
 
 ua::PeerFlags peer_flags(const ua_ctx* ctx) {

@@ -28,13 +28,15 @@ struct ua_ctx {
   };
   std::vector<Rec> pending;
   std::vector<cudaEvent_t> pool;
-  // NVLink peer-store all-to-all (UA_A2A_PEER): library-owned buffers, CUDA IPC
-  // mapped on every rank (peer[k] = rank k's copy, peer[rank] = local).
+  // NVLink peer-store all-to-all (UA_A2A_PEER): library-owned buffers in NCCL
+  // symmetric memory (ncclMemAlloc + ncclCommWindowRegister), load/store-accessible
+  // from every rank (peer[k] = rank k's copy, peer[rank] = local).
   int a2a_mode = UA_A2A_NCCL;
   int deterministic = 0;  // ua_ctx_set_deterministic: query-stationary dQ, no cross-CTA reduction
   struct PeerBuf {
     void* local = nullptr;
     size_t bytes = 0;
+    ncclWindow_t win = nullptr;
     void* peer[ua::kMaxPeers] = {};
   };
   PeerBuf flags, fwd_in, fwd_out, bwd_in, bwd_out;
@@ -63,6 +65,8 @@ ua_status fail(ua_status s, const char* fmt, ...);
 void layer_release(ua_ctx* ctx);
 // UA_OK if the current device is an sm_100 GPU, else UA_ERR_UNSUPPORTED (no CPU fallback).
 ua_status check_device();
+// Writes the P per-rank addresses of window w (ncclGetPeerPointer) to out_dev[0..P) (kernels/nccl_window.cu).
+cudaError_t launch_lsa_ptrs(ncclWindow_t w, int P, void** out_dev, cudaStream_t stream);
 }  // namespace ua_internal
 
 #define UA_CUDA(expr)                                                                                    \

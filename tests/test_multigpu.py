@@ -75,7 +75,7 @@ def test_ulysses_p_way(P):
     """Every Ulysses case at this P, both transports, default and deterministic backward:
     P-way forward == P = 1 bitwise, deterministic P-way grads == P = 1 bitwise,
     oracle gates, call / byte law, head-limit error on every rank without a hang."""
-    # the CUDA-IPC peer transport has run on hardware at P <= 4 (gpurun offers <= 4 GPUs); at P = 8 it
+    # the NVLink peer transport (NCCL windows) has run on hardware at P <= 4 (gpurun offers <= 4 GPUs); at P = 8 it
     # joins the default suite's cases only with UA_MGPU_FULL=1 (its P = 8 index maths is covered on
     # one GPU by tests/test_layout_gpu.py)
     modes = ("nccl", "peer") if (P <= 4 or FULL) else ("nccl",)
