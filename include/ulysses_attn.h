@@ -82,7 +82,10 @@ ua_status ua_workspace_size(int64_t B, int64_t N, int H, int D, int P, size_t* f
  * ua_ctx_create: binds the calling thread to `cuda_device` and, for P > 1,
  * creates the library's own NCCL communicator (ncclCommInitRank); `uid` is
  * ignored (may be NULL) when P == 1.  The ctx owns that communicator and is
- * released by ua_ctx_destroy. */
+ * released by ua_ctx_destroy.  ua_ctx_create and (once the peer transport has
+ * run) ua_ctx_destroy are collective over the P ranks: the symmetric-memory
+ * windows are registered and deregistered by all ranks together, so every rank
+ * must call them. */
 ua_status ua_get_unique_id(unsigned char uid[128]);
 ua_status ua_ctx_create(const unsigned char* uid, int P, int rank, int cuda_device, ua_ctx** out);
 ua_status ua_ctx_destroy(ua_ctx* ctx);
