@@ -117,26 +117,33 @@ def sample_rows(N, rng, extra=12):
     return np.unique(np.array([r for r in fixed if 0 <= r < N] + list(rng.integers(0, N, extra))))
 
 
+_FULL_REF = {}   # (cfg, head) -> fp64 oracle rows: the c4 reference (minutes of CPU) serves both modes
+
+
 @pytest.mark.slow
-@pytest.mark.parametrize("cfg,head", [("c3", 9), ("c4", 17)])
-def test_bwd_full_size_sampled_rows(ua, ctx, cfg, head):
+@pytest.mark.parametrize("cfg,head,det", [("c3", 9, False), ("c4", 17, False), ("c4", 17, True)])
+def test_bwd_full_size_sampled_rows(ua, ctx, dctx, cfg, head, det):
     """Full-size backward at P = 1 (c3: N = 65,536, D = 128; c4: N = 188,416,
-    D = 64): exact fp64 dK, dV for sampled KEY rows of one head
-    (oracle.attn_bwd_kv_rows, which recomputes every lse_i and Delta_i) and dQ
-    for sampled query rows, element by element (Gate A + relL2 + elementwise)."""
+    D = 64; c4 also in the deterministic mode): exact fp64 dK, dV for sampled
+    KEY rows of one head (oracle.attn_bwd_kv_rows, which recomputes every lse_i
+    and Delta_i) and dQ for sampled query rows, element by element (Gate A +
+    relL2 + elementwise)."""
     c = synth.CONFIGS[cfg]
     B, N, H, D = c["B"], c["N"], c["H"], c["D"]
     q, k, v, do = synth.qkv(B, N, H, D, seed=synth.BASE_SEED, with_do=True)
-    dq, dk, dv = run_fwd_bwd(ua, ctx, q, k, v, do)
+    dq, dk, dv = run_fwd_bwd(ua, dctx if det else ctx, q, k, v, do)
     for t in (dq, dk, dv):
         assert np.isfinite(t).all()
     rows = sample_rows(N, np.random.default_rng(17))
-    qh, kh, vh, doh = (synth.to_f64(t[0, :, head]) for t in (q, k, v, do))
-    dk_ref, dv_ref = oracle.attn_bwd_kv_rows(qh, kh, vh, doh, rows)
+    if (cfg, head) not in _FULL_REF:
+        qh, kh, vh, doh = (synth.to_f64(t[0, :, head]) for t in (q, k, v, do))
+        dk_ref, dv_ref = oracle.attn_bwd_kv_rows(qh, kh, vh, doh, rows)
+        bh = np.array([(0, 0)] * len(rows))
+        dq_ref = oracle.attn_bwd_dq_rows(qh[rows], doh[rows], bh, kh[None, :, None, :], vh[None, :, None, :])
+        _FULL_REF[(cfg, head)] = (dk_ref, dv_ref, dq_ref)
+    dk_ref, dv_ref, dq_ref = _FULL_REF[(cfg, head)]
     gate_grad(dk[0, rows, head], dk_ref)
     gate_grad(dv[0, rows, head], dv_ref)
-    bh = np.array([(0, 0)] * len(rows))
-    dq_ref = oracle.attn_bwd_dq_rows(qh[rows], doh[rows], bh, kh[None, :, None, :], vh[None, :, None, :])
     gate_grad(dq[0, rows, head], dq_ref)
 
 
